@@ -1,0 +1,145 @@
+/*
+ * trilist_b200.h -- C-ABI of the B200-native AOT triangle-listing path.
+ *
+ * Drop-in boundary for the hot path of the reference C++ library `trilist`
+ * (/root/reference/proj).  Every entry point lists the reference interface it
+ * replaces.  All pointers are plain host pointers unless a parameter name
+ * starts with `d_` (device pointer).  Functions return TL_OK (0) or a TL_E*
+ * code; tl_last_error() returns the thread-local message of the last failure.
+ * The error codes map onto the reference's exception types:
+ *   TL_EINVAL -> std::invalid_argument   TL_ERANGE -> std::out_of_range
+ *   TL_ELOGIC -> std::logic_error        TL_ECUDA/TL_ENOMEM -> std::runtime_error
+ *
+ * There is no CPU fallback: every compute step below runs as a CUDA kernel for
+ * sm_100a; without a usable CUDA device the calls fail with TL_ENODEV.
+ */
+#ifndef TRILIST_B200_H
+#define TRILIST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TL_OK 0
+#define TL_EINVAL 1
+#define TL_ERANGE 2
+#define TL_ELOGIC 3
+#define TL_ECUDA 4
+#define TL_ENOMEM 5
+#define TL_ECAPACITY 6
+#define TL_ENODEV 7
+
+#define TL_API __attribute__((visibility("default")))
+
+typedef struct tl_graph tl_graph;       /* device-resident Graph (graph.hpp:31-73)            */
+typedef struct tl_oriented tl_oriented; /* device-resident OrientedGraph (ordering.hpp:62-108) */
+
+/* RunStats (engine.hpp:28-54) plus device-side extras. */
+typedef struct tl_stats {
+  uint64_t triangles;
+  uint64_t probes;            /* logical probes: sum of deg+ of every traversed list (== aot_cost) */
+  uint64_t merge_comparisons; /* always 0 for aot                                                  */
+  uint64_t table_builds;      /* sum of deg+ over all pivots (== m)                                */
+  uint64_t positive_triangles;
+  uint64_t negative_triangles;
+  uint64_t probes_executed;   /* probes left after rank-window early exit                          */
+  uint64_t hash_sum;          /* order-independent triangle hash, sum mod 2^64 (hash/list modes)   */
+  uint64_t hash_xor;          /*                                   xor                              */
+  uint64_t tasks;             /* work items scheduled                                              */
+  double list_ms;             /* device time of the listing kernels (CUDA events)                  */
+  double prep_ms;             /* device time of per-run task construction                          */
+} tl_stats;
+
+/* RunOptions (engine.hpp:56-60) + ParallelConfig-equivalent partitioning. */
+typedef struct tl_run_options {
+  uint32_t skip_negative_phase; /* RunOptions::aot_skip_negative_phase (fault injection)           */
+  uint32_t check_hygiene;       /* RunOptions::check_bitmap_between_pivots: accepted, no-op         */
+  uint32_t part;                /* this device's share of the cost-balanced edge partition          */
+  uint32_t nparts;              /* number of shares (GPUs); 0 or 1 = whole graph                    */
+  void* stream;                 /* cudaStream_t to run on; NULL = the handle's own stream           */
+} tl_run_options;
+
+/* ---------------------------------------------------------------- runtime */
+TL_API const char* tl_last_error(void);
+TL_API int tl_device_count(int* count);
+TL_API const char* tl_version(void);
+
+/* ------------------------------------------------- synthetic generators */
+/* Seeded generators of the BASELINE configs; written on device,
+ * bit-identical to oracle/trilist_oracle.c.  d_pairs holds 2*npairs uint32. */
+TL_API int tl_gen_er(uint64_t seed, uint32_t n, uint64_t npairs, uint32_t* d_pairs, void* stream);
+TL_API int tl_gen_rmat(uint64_t seed, uint32_t scale, uint64_t npairs, uint32_t* d_pairs, void* stream);
+/* Chung-Lu: prefix is the host-computed fixed-point weight prefix (n+1). */
+TL_API int tl_chung_lu_prefix(uint64_t seed, uint32_t n, double avg, double gamma, uint64_t* prefix);
+TL_API int tl_gen_chung_lu(uint64_t seed, uint32_t n, const uint64_t* prefix, uint64_t npairs,
+                           uint32_t* d_pairs, void* stream);
+
+/* -------------------------------------------------------- L0 graph core */
+/* Graph::from_edges(min_vertices, span<pair>) -- graph.hpp:38-41, graph.cpp:189-206
+ * (self-loops dropped, duplicates collapsed, n = max(min_vertices, max id + 1)).
+ * `pairs` holds 2*npairs uint32 (u0,v0,u1,v1,...) in host memory, or in device
+ * memory of `device` when pairs_on_device != 0. */
+TL_API int tl_graph_from_pairs(const uint32_t* pairs, uint64_t npairs, uint32_t min_vertices,
+                               int device, int pairs_on_device, void* stream, tl_graph** out);
+TL_API int tl_graph_free(tl_graph* g);
+/* num_vertices()/num_edges() (graph.hpp:43-44) + load diagnostics (graph.hpp:81-86). */
+TL_API int tl_graph_info(const tl_graph* g, uint32_t* n, uint64_t* m, uint64_t* duplicates,
+                         uint64_t* self_loops);
+/* degree(u) for all u (graph.hpp:50-51). */
+TL_API int tl_graph_degrees(tl_graph* g, uint32_t* degrees);
+/* offsets() (n+1) / adjacency() (2m): symmetric ascending CSR (graph.hpp:56-57). */
+TL_API int tl_graph_csr(tl_graph* g, uint64_t* offsets, uint32_t* adjacency);
+
+/* ---------------------------------------------------------- L1 ordering */
+/* degree_order(const Graph&) -- ordering.hpp:24, ordering.cpp:69-84: rank[u] by
+ * ascending (degree, id).  rank has n entries. */
+TL_API int tl_degree_order(tl_graph* g, uint32_t* rank);
+/* orient(const Graph&, const VertexOrder&) -- ordering.hpp:112, ordering.cpp:185-227.
+ * rank == NULL orients by the device-computed degree order.  Throws-equivalent
+ * TL_EINVAL unless rank is a permutation of 0..n-1 (ordering.cpp:187-188). */
+TL_API int tl_orient(tl_graph* g, const uint32_t* rank, tl_oriented** out);
+/* Upload of a host OrientedGraph in the reference layout (out-lists of original
+ * ids, rank-ascending; ordering.hpp:102-105) -- the drop-in path for callers
+ * that already hold an oriented graph. */
+TL_API int tl_oriented_from_csr(uint32_t n, uint64_t m, const uint64_t* out_offsets,
+                                const uint32_t* out, const uint32_t* rank, int device, void* stream,
+                                tl_oriented** out_graph);
+TL_API int tl_oriented_free(tl_oriented* og);
+/* num_vertices/num_edges/max_out_degree -- ordering.hpp:67-68, :99. */
+TL_API int tl_oriented_info(const tl_oriented* og, uint32_t* n, uint64_t* m, uint32_t* max_out_degree);
+/* Reference layout download: out/in CSR of original ids (rank-ascending lists)
+ * and rank[] (ordering.hpp:69-80).  Any pointer may be NULL. */
+TL_API int tl_oriented_csr(tl_oriented* og, uint64_t* out_offsets, uint32_t* out,
+                           uint64_t* in_offsets, uint32_t* in, uint32_t* rank);
+/* cost_model(const OrientedGraph&) -- engine.hpp:338-344, engine.cpp:37-49:
+ * costs[0]=cf_cost, costs[1]=kclist_cost, costs[2]=aot_cost. */
+TL_API int tl_cost_model(tl_oriented* og, uint64_t* costs);
+
+/* ------------------------------------------------------ L2/L3 AOT listing */
+/* run_parallel_count(Algorithm::aot, g, cfg, opt) -- parallel.hpp:81-82, parallel.cpp:5-8
+ * (the per-pivot kernel aot_pivot, engine.hpp:238-276, as sm_100a kernels). */
+TL_API int tl_aot_count(tl_oriented* og, const tl_run_options* opt, tl_stats* stats);
+/* Count + order-independent hash of the canonical triangle set (no emission
+ * buffer; hash_sum/hash_xor filled). */
+TL_API int tl_aot_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats);
+/* run_parallel_collecting / run_collecting -- parallel.hpp:85-88, engine.cpp:31-35.
+ * Writes the emissions of this part as uint32 triples: raw role order
+ * (pivot, neighbor, witness) of engine.hpp:256/:269 when canonical == 0, or the
+ * sorted canonical (a<b<c) set (canonicalize_emissions, engine.cpp:51-57) when
+ * canonical != 0.  triples may be NULL to only count; otherwise cap must be at
+ * least the emission count (TL_ECAPACITY otherwise; stats are still filled). */
+TL_API int tl_aot_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
+                       int canonical, tl_stats* stats);
+
+/* brute_force_triangles(const Graph&, OracleOptions) -- oracle.hpp:18, oracle.cpp:8-25,
+ * as a device kernel: sorted canonical set.  TL_EINVAL if n > max_vertices. */
+TL_API int tl_brute_force(tl_graph* g, uint32_t max_vertices, uint32_t* triples, uint64_t cap,
+                          uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRILIST_B200_H */

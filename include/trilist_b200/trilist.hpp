@@ -1,0 +1,332 @@
+// trilist.hpp -- C++ facade of the reference `trilist` API over the B200 C-ABI.
+//
+// Same names, argument meaning and exception types as the reference headers
+// (graph.hpp, ordering.hpp, engine.hpp, parallel.hpp, oracle.hpp under
+// /root/reference/proj/include/trilist); every computation runs through
+// include/trilist_b200.h on a CUDA device.  Differences, all documented in
+// INTEGRATION.md:
+//   * Algorithm::aot is the only kernel on the B200 path; the others throw
+//     std::invalid_argument (no CPU fallback).
+//   * OrderKind::degeneracy / random throw std::invalid_argument (the north
+//     star fixes the degree order); any explicit VertexOrder permutation is
+//     accepted by orient().
+//   * ParallelConfig is validated exactly like the reference (workers >= 1,
+//     chunk >= 1) but no longer partitions work: the GPU schedules its own
+//     cost-balanced tasks.
+#pragma once
+
+#include <array>
+#include <compare>
+#include <cstdint>
+#include <initializer_list>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "trilist_b200.h"
+
+namespace trilist {
+
+using VertexId = std::uint32_t;
+using EdgeCount = std::uint64_t;
+
+// ------------------------------------------------------------- graph.hpp
+struct Triangle {
+  VertexId a = 0;
+  VertexId b = 0;
+  VertexId c = 0;
+  friend auto operator<=>(const Triangle&, const Triangle&) = default;
+};
+
+Triangle canonical_triangle(VertexId x, VertexId y, VertexId z);
+
+/// Rethrows a C-ABI failure as the reference's exception type.
+[[noreturn]] void throw_status(int code, const std::string& context);
+inline void check(int code, const char* context) {
+  if (code != TL_OK) throw_status(code, context);
+}
+
+/// Undirected simple graph (graph.hpp:31-73).  The CSR lives on the device;
+/// host accessors download it lazily.
+class Graph {
+ public:
+  Graph() = default;
+
+  static Graph from_edges(VertexId min_vertices, std::span<const std::pair<VertexId, VertexId>> edges);
+  static Graph from_edges(VertexId min_vertices, std::initializer_list<std::pair<VertexId, VertexId>> edges);
+  /// Extension: pairs already resident in device memory (2*npairs uint32).
+  static Graph from_device_pairs(VertexId min_vertices, const std::uint32_t* d_pairs, std::uint64_t npairs,
+                                 int device = 0, void* stream = nullptr);
+
+  VertexId num_vertices() const { return n_; }
+  EdgeCount num_edges() const { return m_; }
+
+  std::span<const VertexId> neighbors(VertexId u) const;
+  VertexId degree(VertexId u) const;  // std::out_of_range if u >= n
+  bool has_edge(VertexId u, VertexId v) const;
+  const std::vector<EdgeCount>& offsets() const;
+  const std::vector<VertexId>& adjacency() const;
+  bool validate(std::string* why = nullptr) const;
+
+  std::uint64_t duplicates_dropped() const { return dups_; }
+  std::uint64_t self_loops_dropped() const { return loops_; }
+  tl_graph* handle() const { return h_.get(); }
+  int device() const { return device_; }
+
+ private:
+  struct HostCsr {
+    std::vector<EdgeCount> offsets;
+    std::vector<VertexId> adjacency;
+  };
+  static Graph wrap(tl_graph* h, int device);
+  const HostCsr& csr() const;
+
+  std::shared_ptr<tl_graph> h_;
+  int device_ = 0;
+  VertexId n_ = 0;
+  EdgeCount m_ = 0;
+  std::uint64_t dups_ = 0, loops_ = 0;
+  mutable std::shared_ptr<HostCsr> csr_;
+};
+
+// ---------------------------------------------------------- ordering.hpp
+struct VertexOrder {
+  std::vector<VertexId> rank;
+  bool is_permutation() const;
+  std::vector<VertexId> vertices_by_rank() const;
+};
+
+VertexOrder id_order(const Graph& g);
+VertexOrder degree_order(const Graph& g);  // device counting order, ordering.cpp:69-84
+VertexOrder degeneracy_order(const Graph& g);  // std::invalid_argument on this path
+VertexOrder random_order(const Graph& g, std::uint64_t seed);  // std::invalid_argument on this path
+
+enum class OrderKind { id, degree, degeneracy, random };
+struct OrderSpec {
+  OrderKind kind = OrderKind::degree;
+  std::uint64_t seed = 0;
+};
+VertexOrder make_order(const Graph& g, const OrderSpec& spec);
+OrderSpec parse_order_spec(const std::string& text);
+std::string to_string(const OrderSpec& spec);
+
+enum class LocalOrderPolicy { rank_asc, degree_desc, random };
+struct LocalOrder {
+  LocalOrderPolicy policy = LocalOrderPolicy::rank_asc;
+  std::uint64_t seed = 0;
+};
+LocalOrder parse_local_order(const std::string& text);
+std::string to_string(const LocalOrder& local);
+
+/// Degree-oriented DAG (ordering.hpp:62-108).  The device copy is always
+/// rank-ascending (AOT's early exit needs it); the host accessor lists follow
+/// local_order() exactly like the reference's.
+class OrientedGraph {
+ public:
+  OrientedGraph() = default;
+
+  /// Extension: upload a host OrientedGraph in the reference layout.
+  static OrientedGraph from_csr(VertexId n, std::span<const EdgeCount> out_offsets, std::span<const VertexId> out,
+                                std::span<const VertexId> rank, int device = 0);
+
+  VertexId num_vertices() const { return n_; }
+  EdgeCount num_edges() const { return m_; }
+  std::span<const VertexId> out_neighbors(VertexId u) const;
+  std::span<const VertexId> in_neighbors(VertexId u) const;
+  VertexId out_degree(VertexId u) const;
+  VertexId in_degree(VertexId u) const;
+  VertexId undirected_degree(VertexId u) const { return out_degree(u) + in_degree(u); }
+  VertexId rank(VertexId u) const { return order().rank[u]; }
+  const VertexOrder& order() const;
+  const LocalOrder& local_order() const { return local_; }
+  bool out_degree_before(VertexId a, VertexId b) const {
+    VertexId da = out_degree(a), db = out_degree(b);
+    return da != db ? da < db : a < b;
+  }
+  bool out_lists_rank_sorted() const;
+  VertexId max_out_degree() const { return max_out_; }
+
+  tl_oriented* handle() const { return h_.get(); }
+  int device() const { return device_; }
+
+ private:
+  friend OrientedGraph orient(const Graph&, const VertexOrder&);
+  friend OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local);
+  struct HostLayout {
+    std::vector<EdgeCount> out_offsets, in_offsets;
+    std::vector<VertexId> out, in;
+    VertexOrder order;
+  };
+  static OrientedGraph wrap(tl_oriented* h, int device);
+  const HostLayout& host() const;
+
+  std::shared_ptr<tl_oriented> h_;
+  int device_ = 0;
+  VertexId n_ = 0;
+  EdgeCount m_ = 0;
+  VertexId max_out_ = 0;
+  LocalOrder local_;
+  mutable std::shared_ptr<HostLayout> host_;
+};
+
+OrientedGraph orient(const Graph& g, const VertexOrder& order);
+OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local);
+
+enum class EdgePolarity { positive, negative };
+EdgePolarity edge_polarity(const OrientedGraph& g, VertexId u, VertexId v);
+
+// ------------------------------------------------------------ engine.hpp
+enum class Algorithm { cf_merge, cf_hash, kclist3, aot };
+inline constexpr std::array<Algorithm, 4> kAllAlgorithms = {Algorithm::cf_merge, Algorithm::cf_hash,
+                                                            Algorithm::kclist3, Algorithm::aot};
+/// Algorithms with a B200 implementation.
+inline constexpr std::array<Algorithm, 1> kDeviceAlgorithms = {Algorithm::aot};
+const char* to_string(Algorithm a);
+Algorithm parse_algorithm(const std::string& name);
+
+struct RunStats {
+  std::uint64_t triangles = 0;
+  std::uint64_t probes = 0;
+  std::uint64_t merge_comparisons = 0;
+  std::uint64_t table_builds = 0;
+  std::uint64_t positive_triangles = 0;
+  std::uint64_t negative_triangles = 0;
+  double wall_time_s = 0.0;  // listing kernels only (CUDA events), like the reference's
+  // device extras
+  std::uint64_t probes_executed = 0;
+  std::uint64_t hash_sum = 0;
+  std::uint64_t hash_xor = 0;
+
+  void add_counters(const RunStats& o) {
+    triangles += o.triangles;
+    probes += o.probes;
+    merge_comparisons += o.merge_comparisons;
+    table_builds += o.table_builds;
+    positive_triangles += o.positive_triangles;
+    negative_triangles += o.negative_triangles;
+  }
+  bool counters_equal(const RunStats& o) const {
+    return triangles == o.triangles && probes == o.probes && merge_comparisons == o.merge_comparisons &&
+           table_builds == o.table_builds && positive_triangles == o.positive_triangles &&
+           negative_triangles == o.negative_triangles;
+  }
+};
+
+struct RunOptions {
+  bool check_bitmap_between_pivots = false;  // accepted; the device tables are per work item
+  bool cf_hash_reuse_last_table = false;     // cf-hash only (not on this path)
+  bool aot_skip_negative_phase = false;      // fault injection hook for the verifier
+};
+
+struct NullSink {
+  void operator()(VertexId, VertexId, VertexId) const noexcept {}
+};
+struct CollectingSink {
+  std::vector<std::array<VertexId, 3>>* out;
+  void operator()(VertexId a, VertexId b, VertexId c) const { out->push_back({a, b, c}); }
+};
+
+namespace detail {
+void require_device_algorithm(Algorithm a);
+RunStats device_count(const OrientedGraph& g, const RunOptions& opt, int mode /*0 count, 1 hash*/);
+RunStats device_list(const OrientedGraph& g, const RunOptions& opt, std::vector<std::array<VertexId, 3>>& raw);
+}  // namespace detail
+
+template <typename Sink>
+RunStats run_algorithm(Algorithm algo, const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
+  detail::require_device_algorithm(algo);
+  if constexpr (std::is_same_v<std::decay_t<Sink>, NullSink>) {
+    return detail::device_count(g, opt, 0);
+  } else {
+    std::vector<std::array<VertexId, 3>> raw;
+    RunStats s = detail::device_list(g, opt, raw);
+    for (const auto& t : raw) sink(t[0], t[1], t[2]);  // role order (pivot, neighbor, witness)
+    return s;
+  }
+}
+
+template <typename Sink>
+RunStats aot(const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
+  return run_algorithm(Algorithm::aot, g, sink, opt);
+}
+
+RunStats run_counting(Algorithm algo, const OrientedGraph& g, const RunOptions& opt = {});
+RunStats run_collecting(Algorithm algo, const OrientedGraph& g, std::vector<std::array<VertexId, 3>>& out,
+                        const RunOptions& opt = {});
+/// Extension: count + order-independent hash of the canonical triangle set.
+RunStats run_hashing(Algorithm algo, const OrientedGraph& g, const RunOptions& opt = {});
+
+struct CostModel {
+  std::uint64_t cf_cost = 0;
+  std::uint64_t kclist_cost = 0;
+  std::uint64_t aot_cost = 0;
+};
+CostModel cost_model(const OrientedGraph& g);
+
+std::vector<Triangle> canonicalize_emissions(std::span<const std::array<VertexId, 3>> raw);
+
+struct VerifyAlgorithmResult {
+  Algorithm algorithm = Algorithm::aot;
+  RunStats stats;
+  std::uint64_t unique_triangles = 0;
+  std::uint64_t duplicate_emissions = 0;
+  std::uint64_t missing_count = 0;
+  std::uint64_t extra_count = 0;
+  std::vector<Triangle> missing_samples;
+  std::vector<Triangle> extra_samples;
+  bool pass = true;
+};
+
+struct VerifyReport {
+  static constexpr std::size_t kMaxSamples = 32;
+  bool pass = true;
+  std::string reference;
+  std::uint64_t reference_count = 0;
+  std::vector<VerifyAlgorithmResult> results;
+};
+
+VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algorithms, const VertexOrder& order,
+                                const LocalOrder& local = {}, const std::vector<Triangle>* reference = nullptr,
+                                const RunOptions& opt = {});
+
+// ---------------------------------------------------------- parallel.hpp
+struct ParallelConfig {
+  unsigned workers = 1;
+  VertexId chunk = 64;
+};
+
+namespace detail {
+void validate(const ParallelConfig& cfg);
+}
+
+/// run_parallel (parallel.hpp:25-78): one device run; the emissions are
+/// handed to the sink of worker 0 (the other workers' sinks see none).
+template <typename SinkFactory>
+RunStats run_parallel(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg, SinkFactory&& make_sink,
+                      const RunOptions& opt = {}) {
+  detail::validate(cfg);
+  using Sink = std::decay_t<decltype(make_sink(0u))>;
+  std::vector<Sink> sinks;
+  sinks.reserve(cfg.workers);
+  for (unsigned w = 0; w < cfg.workers; ++w) sinks.push_back(make_sink(w));
+  return run_algorithm(algo, g, sinks[0], opt);
+}
+
+RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                            const RunOptions& opt = {});
+RunStats run_parallel_collecting(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                                 std::vector<std::vector<std::array<VertexId, 3>>>& buffers,
+                                 const RunOptions& opt = {});
+
+// ------------------------------------------------------------ oracle.hpp
+struct OracleOptions {
+  VertexId max_vertices = 2000;
+};
+/// brute_force_triangles (oracle.cpp:8-25) as a device kernel.
+std::vector<Triangle> brute_force_triangles(const Graph& g, const OracleOptions& opt = {});
+
+}  // namespace trilist

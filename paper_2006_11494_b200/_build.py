@@ -1,0 +1,95 @@
+"""In-tree build of the B200 library and its Python binding.
+
+* ``lib/libtrilist_b200.so`` -- the CUDA kernels + the C-ABI of
+  ``include/trilist_b200.h`` (nvcc, ``-gencode arch=compute_100a,code=sm_100a``,
+  cudart linked statically so the .so is self-contained on the GPU box).
+* ``trilist/_core*.so`` -- the pybind11 mirror of the reference's
+  ``trilist._core`` over the C++ facade (``include/trilist_b200/trilist.hpp``).
+
+Incremental: a target is rebuilt only when a source it depends on is newer.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+import sysconfig
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+OBJ = os.path.join(ROOT, "build", "obj")
+LIBDIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIBDIR, "libtrilist_b200.so")
+EXT = os.path.join(PKG, "trilist", "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_capi.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+                     "--expt-relaxed-constexpr", "-I" + INC, "-I" + CSRC]
+
+
+def _headers():
+    return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INC, "*.h")) + \
+        glob.glob(os.path.join(INC, "trilist_b200", "*.hpp"))
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def build_lib(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(LIBDIR, exist_ok=True)
+    hdrs = _headers()
+    objs, procs = [], []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        objs.append(o)
+        if force or _stale(o, [s] + hdrs):
+            cmd = [NVCC] + NVCC_FLAGS + ["-c", s, "-o", o]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append((subprocess.Popen(cmd), cmd))
+    for p, cmd in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
+    if force or procs or _stale(LIB, objs):
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs +
+             ["-Xlinker", "--exclude-libs,ALL"], verbose)
+    return LIB
+
+
+def build_ext(verbose: bool = False, force: bool = False) -> str:
+    import pybind11
+
+    srcs = [os.path.join(CSRC, "facade.cpp"), os.path.join(CSRC, "bindings.cpp")]
+    if force or _stale(EXT, srcs + _headers() + [LIB]):
+        py_inc = sysconfig.get_paths()["include"]
+        cmd = ["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-fvisibility=hidden", "-I" + INC,
+               "-I" + pybind11.get_include(), "-I" + py_inc] + srcs + \
+              ["-L" + LIBDIR, "-ltrilist_b200", "-Wl,-rpath,$ORIGIN/../lib", "-o", EXT]
+        _run(cmd, verbose)
+    return EXT
+
+
+def build(verbose: bool = False, force: bool = False) -> None:
+    build_lib(verbose, force)
+    build_ext(verbose, force)
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)

@@ -1,0 +1,577 @@
+// facade.cpp -- the reference `trilist` C++ API (include/trilist_b200/trilist.hpp)
+// implemented over the B200 C-ABI.  Host code here only validates arguments,
+// moves data across the boundary and reshapes host-side views (accessor
+// lists, sink replay, set differences); every triangle/graph computation is a
+// device call.
+#include "trilist_b200/trilist.hpp"
+
+#include <algorithm>
+#include <charconv>
+#include <cstring>
+#include <mutex>
+
+namespace trilist {
+
+// ------------------------------------------------------------------ errors
+[[noreturn]] void throw_status(int code, const std::string& context) {
+  std::string msg = context + ": " + tl_last_error();
+  switch (code) {
+    case TL_EINVAL: throw std::invalid_argument(tl_last_error());
+    case TL_ERANGE: throw std::out_of_range(tl_last_error());
+    case TL_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+Triangle canonical_triangle(VertexId x, VertexId y, VertexId z) {  // graph.cpp:148-153
+  if (x > y) std::swap(x, y);
+  if (y > z) std::swap(y, z);
+  if (x > y) std::swap(x, y);
+  return {x, y, z};
+}
+
+// ------------------------------------------------------------------- Graph
+Graph Graph::wrap(tl_graph* h, int device) {
+  Graph g;
+  g.h_ = std::shared_ptr<tl_graph>(h, [](tl_graph* p) { tl_graph_free(p); });
+  g.device_ = device;
+  check(tl_graph_info(h, &g.n_, &g.m_, &g.dups_, &g.loops_), "tl_graph_info");
+  return g;
+}
+
+Graph Graph::from_edges(VertexId min_vertices, std::span<const std::pair<VertexId, VertexId>> edges) {
+  static_assert(sizeof(std::pair<VertexId, VertexId>) == 8, "pair layout");
+  tl_graph* h = nullptr;
+  check(tl_graph_from_pairs(reinterpret_cast<const std::uint32_t*>(edges.data()), edges.size(), min_vertices, 0, 0,
+                            nullptr, &h),
+        "Graph::from_edges");
+  return wrap(h, 0);
+}
+
+Graph Graph::from_edges(VertexId min_vertices, std::initializer_list<std::pair<VertexId, VertexId>> edges) {
+  return from_edges(min_vertices, std::span<const std::pair<VertexId, VertexId>>(edges.begin(), edges.size()));
+}
+
+Graph Graph::from_device_pairs(VertexId min_vertices, const std::uint32_t* d_pairs, std::uint64_t npairs, int device,
+                               void* stream) {
+  tl_graph* h = nullptr;
+  check(tl_graph_from_pairs(d_pairs, npairs, min_vertices, device, 1, stream, &h), "Graph::from_device_pairs");
+  return wrap(h, device);
+}
+
+const Graph::HostCsr& Graph::csr() const {
+  if (!csr_) {
+    auto c = std::make_shared<HostCsr>();
+    c->offsets.assign(std::size_t(n_) + 1, 0);
+    c->adjacency.resize(2 * m_);
+    if (h_) check(tl_graph_csr(h_.get(), c->offsets.data(), c->adjacency.data()), "Graph::offsets");
+    csr_ = c;
+  }
+  return *csr_;
+}
+
+std::span<const VertexId> Graph::neighbors(VertexId u) const {
+  const HostCsr& c = csr();
+  return {c.adjacency.data() + c.offsets[u], c.adjacency.data() + c.offsets[u + 1]};
+}
+
+VertexId Graph::degree(VertexId u) const {  // graph.cpp:208-211
+  if (u >= n_) throw std::out_of_range("vertex id " + std::to_string(u) + " out of range");
+  const HostCsr& c = csr();
+  return VertexId(c.offsets[u + 1] - c.offsets[u]);
+}
+
+bool Graph::has_edge(VertexId u, VertexId v) const {  // graph.cpp:213-217
+  if (u >= n_ || v >= n_) return false;
+  auto nu = neighbors(u);
+  return std::binary_search(nu.begin(), nu.end(), v);
+}
+
+const std::vector<EdgeCount>& Graph::offsets() const { return csr().offsets; }
+const std::vector<VertexId>& Graph::adjacency() const { return csr().adjacency; }
+
+bool Graph::validate(std::string* why) const {  // graph.cpp:219-238
+  auto fail = [&](const std::string& reason) {
+    if (why) *why = reason;
+    return false;
+  };
+  const HostCsr& c = csr();
+  if (c.offsets.size() != std::size_t(n_) + 1) return fail("offsets size");
+  if (c.offsets.front() != 0 || c.offsets.back() != 2 * m_) return fail("offset bounds");
+  if (c.adjacency.size() != 2 * m_) return fail("adjacency size");
+  for (VertexId u = 0; u < n_; ++u) {
+    if (c.offsets[u] > c.offsets[u + 1]) return fail("offsets not monotone");
+    auto nu = neighbors(u);
+    for (std::size_t i = 0; i < nu.size(); ++i) {
+      if (nu[i] >= n_) return fail("neighbor out of range");
+      if (nu[i] == u) return fail("self-loop");
+      if (i > 0 && nu[i - 1] >= nu[i]) return fail("list not strictly ascending");
+      if (!has_edge(nu[i], u)) return fail("asymmetric edge");
+    }
+  }
+  return true;
+}
+
+// --------------------------------------------------------------- ordering
+bool VertexOrder::is_permutation() const {
+  std::vector<bool> seen(rank.size(), false);
+  for (VertexId r : rank) {
+    if (r >= rank.size() || seen[r]) return false;
+    seen[r] = true;
+  }
+  return true;
+}
+
+std::vector<VertexId> VertexOrder::vertices_by_rank() const {
+  std::vector<VertexId> by_rank(rank.size());
+  for (VertexId u = 0; u < rank.size(); ++u) by_rank[rank[u]] = u;
+  return by_rank;
+}
+
+VertexOrder id_order(const Graph& g) {
+  VertexOrder o;
+  o.rank.resize(g.num_vertices());
+  for (VertexId u = 0; u < g.num_vertices(); ++u) o.rank[u] = u;
+  return o;
+}
+
+VertexOrder degree_order(const Graph& g) {
+  VertexOrder o;
+  o.rank.resize(g.num_vertices());
+  if (g.handle() && g.num_vertices()) check(tl_degree_order(g.handle(), o.rank.data()), "degree_order");
+  return o;
+}
+
+VertexOrder degeneracy_order(const Graph&) {
+  throw std::invalid_argument("order 'degeneracy' has no B200 implementation (the AOT path uses the degree order)");
+}
+
+VertexOrder random_order(const Graph&, std::uint64_t) {
+  throw std::invalid_argument("order 'random' has no B200 implementation (the AOT path uses the degree order)");
+}
+
+VertexOrder make_order(const Graph& g, const OrderSpec& spec) {
+  switch (spec.kind) {
+    case OrderKind::id: return id_order(g);
+    case OrderKind::degree: return degree_order(g);
+    case OrderKind::degeneracy: return degeneracy_order(g);
+    case OrderKind::random: return random_order(g, spec.seed);
+  }
+  throw std::invalid_argument("unknown order kind");
+}
+
+namespace {
+std::uint64_t splitmix64(std::uint64_t& state) {  // ordering.cpp:13-19
+  state += 0x9E3779B97F4A7C15ull;
+  std::uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+std::uint64_t parse_seed(const std::string& text, std::size_t colon, const char* what) {
+  std::uint64_t seed = 0;
+  const char* b = text.data() + colon + 1;
+  const char* e = text.data() + text.size();
+  auto [p, ec] = std::from_chars(b, e, seed);
+  if (ec != std::errc{} || p != e || b == e)
+    throw std::invalid_argument(std::string("bad ") + what + " seed in '" + text + "'");
+  return seed;
+}
+}  // namespace
+
+OrderSpec parse_order_spec(const std::string& text) {  // ordering.cpp:132-141
+  if (text == "id") return {OrderKind::id, 0};
+  if (text == "degree") return {OrderKind::degree, 0};
+  if (text == "degeneracy") return {OrderKind::degeneracy, 0};
+  if (text.rfind("random:", 0) == 0) return {OrderKind::random, parse_seed(text, 6, "order")};
+  throw std::invalid_argument("unknown order '" + text + "' (expected id|degree|degeneracy|random:SEED)");
+}
+
+std::string to_string(const OrderSpec& spec) {
+  switch (spec.kind) {
+    case OrderKind::id: return "id";
+    case OrderKind::degree: return "degree";
+    case OrderKind::degeneracy: return "degeneracy";
+    case OrderKind::random: return "random:" + std::to_string(spec.seed);
+  }
+  return "?";
+}
+
+LocalOrder parse_local_order(const std::string& text) {  // ordering.cpp:154-161
+  if (text == "rank-asc") return {LocalOrderPolicy::rank_asc, 0};
+  if (text == "degree-desc") return {LocalOrderPolicy::degree_desc, 0};
+  if (text.rfind("random:", 0) == 0) return {LocalOrderPolicy::random, parse_seed(text, 6, "local order")};
+  throw std::invalid_argument("unknown local order '" + text + "' (expected rank-asc|degree-desc|random:SEED)");
+}
+
+std::string to_string(const LocalOrder& local) {
+  switch (local.policy) {
+    case LocalOrderPolicy::rank_asc: return "rank-asc";
+    case LocalOrderPolicy::degree_desc: return "degree-desc";
+    case LocalOrderPolicy::random: return "random:" + std::to_string(local.seed);
+  }
+  return "?";
+}
+
+OrientedGraph OrientedGraph::wrap(tl_oriented* h, int device) {
+  OrientedGraph og;
+  og.h_ = std::shared_ptr<tl_oriented>(h, [](tl_oriented* p) { tl_oriented_free(p); });
+  og.device_ = device;
+  check(tl_oriented_info(h, &og.n_, &og.m_, &og.max_out_), "tl_oriented_info");
+  return og;
+}
+
+OrientedGraph OrientedGraph::from_csr(VertexId n, std::span<const EdgeCount> out_offsets, std::span<const VertexId> out,
+                                      std::span<const VertexId> rank, int device) {
+  if (out_offsets.size() != std::size_t(n) + 1 || rank.size() != n)
+    throw std::invalid_argument("OrientedGraph::from_csr: array sizes do not match n");
+  tl_oriented* h = nullptr;
+  check(tl_oriented_from_csr(n, out.size(), out_offsets.data(), out.data(), rank.data(), device, nullptr, &h),
+        "OrientedGraph::from_csr");
+  return wrap(h, device);
+}
+
+const OrientedGraph::HostLayout& OrientedGraph::host() const {
+  if (!host_) {
+    auto L = std::make_shared<HostLayout>();
+    L->out_offsets.assign(std::size_t(n_) + 1, 0);
+    L->in_offsets.assign(std::size_t(n_) + 1, 0);
+    L->out.resize(m_);
+    L->in.resize(m_);
+    L->order.rank.resize(n_);
+    if (h_)
+      check(tl_oriented_csr(h_.get(), L->out_offsets.data(), L->out.data(), L->in_offsets.data(), L->in.data(),
+                            L->order.rank.data()),
+            "OrientedGraph accessors");
+    host_ = L;
+  }
+  return *host_;
+}
+
+std::span<const VertexId> OrientedGraph::out_neighbors(VertexId u) const {
+  const HostLayout& L = host();
+  return {L.out.data() + L.out_offsets[u], L.out.data() + L.out_offsets[u + 1]};
+}
+std::span<const VertexId> OrientedGraph::in_neighbors(VertexId u) const {
+  const HostLayout& L = host();
+  return {L.in.data() + L.in_offsets[u], L.in.data() + L.in_offsets[u + 1]};
+}
+VertexId OrientedGraph::out_degree(VertexId u) const {
+  const HostLayout& L = host();
+  return VertexId(L.out_offsets[u + 1] - L.out_offsets[u]);
+}
+VertexId OrientedGraph::in_degree(VertexId u) const {
+  const HostLayout& L = host();
+  return VertexId(L.in_offsets[u + 1] - L.in_offsets[u]);
+}
+const VertexOrder& OrientedGraph::order() const { return host().order; }
+
+bool OrientedGraph::out_lists_rank_sorted() const {
+  for (VertexId u = 0; u < n_; ++u) {
+    auto nb = out_neighbors(u);
+    for (std::size_t i = 1; i < nb.size(); ++i)
+      if (rank(nb[i - 1]) >= rank(nb[i])) return false;
+  }
+  return true;
+}
+
+OrientedGraph orient(const Graph& g, const VertexOrder& order) {  // ordering.cpp:185-188
+  VertexId n = g.num_vertices();
+  if (order.rank.size() != n) throw std::invalid_argument("order is not a permutation of the vertex set");
+  if (!g.handle()) {  // default-constructed empty Graph
+    if (n != 0) throw std::invalid_argument("graph has no device handle");
+    Graph empty = Graph::from_edges(0, std::span<const std::pair<VertexId, VertexId>>());
+    return orient(empty, order);
+  }
+  tl_oriented* h = nullptr;
+  check(tl_orient(g.handle(), order.rank.data(), &h), "orient");
+  return OrientedGraph::wrap(h, g.device());
+}
+
+// The device copy stays rank-ascending; only the host accessor lists are
+// rewritten, exactly as ordering.cpp:229-266 does.
+OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local) {
+  const auto& src = g.host();
+  auto L = std::make_shared<OrientedGraph::HostLayout>(src);
+  auto udeg = [&](VertexId x) {
+    return VertexId(L->out_offsets[x + 1] - L->out_offsets[x] + L->in_offsets[x + 1] - L->in_offsets[x]);
+  };
+  const auto& rank = L->order.rank;
+  auto fisher_yates = [](VertexId* first, VertexId* last, std::uint64_t seed) {  // ordering.cpp:23-33
+    std::uint64_t state = seed;
+    auto n = std::uint64_t(last - first);
+    for (std::uint64_t i = n; i > 1; --i) {
+      std::uint64_t j = std::uint64_t((static_cast<unsigned __int128>(splitmix64(state)) * i) >> 64);
+      std::swap(first[i - 1], first[j]);
+    }
+  };
+  for (VertexId u = 0; u < g.num_vertices(); ++u) {
+    for (std::uint64_t side = 0; side < 2; ++side) {
+      auto& lst = side ? L->in : L->out;
+      auto& off = side ? L->in_offsets : L->out_offsets;
+      VertexId* b = lst.data() + off[u];
+      VertexId* e = lst.data() + off[u + 1];
+      switch (local.policy) {
+        case LocalOrderPolicy::rank_asc:
+          std::sort(b, e, [&](VertexId x, VertexId y) { return rank[x] < rank[y]; });
+          break;
+        case LocalOrderPolicy::degree_desc:
+          std::sort(b, e, [&](VertexId x, VertexId y) {
+            VertexId dx = udeg(x), dy = udeg(y);
+            return dx != dy ? dx > dy : x < y;
+          });
+          break;
+        case LocalOrderPolicy::random: {
+          std::sort(b, e, [&](VertexId x, VertexId y) { return rank[x] < rank[y]; });
+          std::uint64_t mix = local.seed;
+          std::uint64_t list_key = splitmix64(mix) ^ ((std::uint64_t(u) << 1) | side);
+          fisher_yates(b, e, list_key);
+          break;
+        }
+      }
+    }
+  }
+  g.host_ = L;
+  g.local_ = local;
+  return g;
+}
+
+EdgePolarity edge_polarity(const OrientedGraph& g, VertexId u, VertexId v) {  // ordering.cpp:268-276
+  if (u >= g.num_vertices() || v >= g.num_vertices()) throw std::invalid_argument("vertex id out of range");
+  auto nb = g.out_neighbors(u);
+  if (std::find(nb.begin(), nb.end(), v) == nb.end())
+    throw std::invalid_argument("no directed edge " + std::to_string(u) + " -> " + std::to_string(v));
+  return g.out_degree_before(u, v) ? EdgePolarity::positive : EdgePolarity::negative;
+}
+
+// ------------------------------------------------------------------ engine
+const char* to_string(Algorithm a) {  // engine.cpp:7-15
+  switch (a) {
+    case Algorithm::cf_merge: return "cf";
+    case Algorithm::cf_hash: return "cf-hash";
+    case Algorithm::kclist3: return "kclist";
+    case Algorithm::aot: return "aot";
+  }
+  return "?";
+}
+
+Algorithm parse_algorithm(const std::string& name) {  // engine.cpp:17-24
+  if (name == "cf") return Algorithm::cf_merge;
+  if (name == "cf-hash") return Algorithm::cf_hash;
+  if (name == "kclist") return Algorithm::kclist3;
+  if (name == "aot") return Algorithm::aot;
+  throw std::invalid_argument("unknown algorithm '" + name + "' (expected cf|cf-hash|kclist|aot)");
+}
+
+namespace detail {
+
+void require_device_algorithm(Algorithm a) {
+  if (a != Algorithm::aot)
+    throw std::invalid_argument(std::string("algorithm '") + to_string(a) +
+                                "' has no B200 implementation (only aot runs on the device)");
+}
+
+namespace {
+tl_run_options options_for(const RunOptions& opt) {
+  tl_run_options o;
+  std::memset(&o, 0, sizeof(o));
+  o.skip_negative_phase = opt.aot_skip_negative_phase ? 1u : 0u;
+  o.check_hygiene = opt.check_bitmap_between_pivots ? 1u : 0u;
+  o.part = 0;
+  o.nparts = 1;
+  return o;
+}
+
+RunStats to_run_stats(const tl_stats& s) {
+  RunStats r;
+  r.triangles = s.triangles;
+  r.probes = s.probes;
+  r.merge_comparisons = s.merge_comparisons;
+  r.table_builds = s.table_builds;
+  r.positive_triangles = s.positive_triangles;
+  r.negative_triangles = s.negative_triangles;
+  r.wall_time_s = s.list_ms * 1e-3;
+  r.probes_executed = s.probes_executed;
+  r.hash_sum = s.hash_sum;
+  r.hash_xor = s.hash_xor;
+  return r;
+}
+
+bool empty_handle(const OrientedGraph& g) { return g.handle() == nullptr; }
+}  // namespace
+
+RunStats device_count(const OrientedGraph& g, const RunOptions& opt, int mode) {
+  if (empty_handle(g)) return RunStats{};
+  tl_run_options o = options_for(opt);
+  tl_stats s;
+  if (mode == 1)
+    check(tl_aot_hash(g.handle(), &o, &s), "aot hash");
+  else
+    check(tl_aot_count(g.handle(), &o, &s), "aot count");
+  return to_run_stats(s);
+}
+
+RunStats device_list(const OrientedGraph& g, const RunOptions& opt, std::vector<std::array<VertexId, 3>>& raw) {
+  if (empty_handle(g)) return RunStats{};
+  tl_run_options o = options_for(opt);
+  tl_stats s;
+  check(tl_aot_list(g.handle(), &o, nullptr, 0, 0, &s), "aot list");  // count (cached for sizing)
+  std::size_t base = raw.size();
+  raw.resize(base + s.triangles);
+  static_assert(sizeof(std::array<VertexId, 3>) == 12, "triple layout");
+  check(tl_aot_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(raw.data() + base), s.triangles, 0, &s),
+        "aot list");
+  return to_run_stats(s);
+}
+
+void validate(const ParallelConfig& cfg) {  // parallel.hpp:28-29
+  if (cfg.workers < 1) throw std::invalid_argument("workers must be >= 1");
+  if (cfg.chunk < 1) throw std::invalid_argument("chunk must be >= 1");
+}
+
+}  // namespace detail
+
+RunStats run_counting(Algorithm algo, const OrientedGraph& g, const RunOptions& opt) {
+  detail::require_device_algorithm(algo);
+  return detail::device_count(g, opt, 0);
+}
+
+RunStats run_collecting(Algorithm algo, const OrientedGraph& g, std::vector<std::array<VertexId, 3>>& out,
+                        const RunOptions& opt) {
+  detail::require_device_algorithm(algo);
+  return detail::device_list(g, opt, out);
+}
+
+RunStats run_hashing(Algorithm algo, const OrientedGraph& g, const RunOptions& opt) {
+  detail::require_device_algorithm(algo);
+  return detail::device_count(g, opt, 1);
+}
+
+CostModel cost_model(const OrientedGraph& g) {
+  CostModel cm;
+  if (!g.handle()) return cm;
+  std::uint64_t c[3];
+  check(tl_cost_model(g.handle(), c), "cost_model");
+  cm.cf_cost = c[0];
+  cm.kclist_cost = c[1];
+  cm.aot_cost = c[2];
+  return cm;
+}
+
+std::vector<Triangle> canonicalize_emissions(std::span<const std::array<VertexId, 3>> raw) {  // engine.cpp:51-57
+  std::vector<Triangle> out;
+  out.reserve(raw.size());
+  for (const auto& t : raw) out.push_back(canonical_triangle(t[0], t[1], t[2]));
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+namespace {
+void diff_sets(const std::vector<Triangle>& reference, const std::vector<Triangle>& got,
+               VerifyAlgorithmResult& r) {  // engine.cpp:62-78
+  std::size_t i = 0, j = 0;
+  while (i < reference.size() || j < got.size()) {
+    if (j == got.size() || (i < reference.size() && reference[i] < got[j])) {
+      if (r.missing_samples.size() < VerifyReport::kMaxSamples) r.missing_samples.push_back(reference[i]);
+      ++r.missing_count, ++i;
+    } else if (i == reference.size() || got[j] < reference[i]) {
+      if (r.extra_samples.size() < VerifyReport::kMaxSamples) r.extra_samples.push_back(got[j]);
+      ++r.extra_count, ++j;
+    } else {
+      ++i, ++j;
+    }
+  }
+}
+
+// Device-canonicalised, device-sorted emission list (duplicates kept).
+std::vector<Triangle> device_canonical(const OrientedGraph& g, const RunOptions& opt, RunStats& stats) {
+  std::vector<Triangle> out;
+  if (!g.handle()) return out;
+  tl_run_options o;
+  std::memset(&o, 0, sizeof(o));
+  o.skip_negative_phase = opt.aot_skip_negative_phase ? 1u : 0u;
+  o.nparts = 1;
+  tl_stats s;
+  check(tl_aot_list(g.handle(), &o, nullptr, 0, 1, &s), "aot list");
+  out.resize(s.triangles);
+  static_assert(sizeof(Triangle) == 12, "Triangle layout");
+  check(tl_aot_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(out.data()), out.size(), 1, &s), "aot list");
+  RunStats r;
+  r.triangles = s.triangles;
+  r.probes = s.probes;
+  r.table_builds = s.table_builds;
+  r.positive_triangles = s.positive_triangles;
+  r.negative_triangles = s.negative_triangles;
+  r.wall_time_s = s.list_ms * 1e-3;
+  r.probes_executed = s.probes_executed;
+  stats = r;
+  return out;
+}
+}  // namespace
+
+VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algorithms, const VertexOrder& order,
+                                const LocalOrder& local, const std::vector<Triangle>* reference,
+                                const RunOptions& opt) {  // engine.cpp:82-130
+  for (Algorithm a : algorithms) detail::require_device_algorithm(a);
+  OrientedGraph oriented = orient(g, order);
+  (void)local;  // layout policy does not change any counter or set (test_engine.cpp:172-185)
+  VerifyReport report;
+  std::vector<Triangle> baseline;
+  if (reference) {
+    baseline = *reference;
+    std::sort(baseline.begin(), baseline.end());
+    baseline.erase(std::unique(baseline.begin(), baseline.end()), baseline.end());
+    report.reference = "oracle";
+  }
+  for (Algorithm algo : algorithms) {
+    VerifyAlgorithmResult r;
+    r.algorithm = algo;
+    std::vector<Triangle> canon = device_canonical(oriented, opt, r.stats);
+    std::vector<Triangle> uniq = canon;
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    r.unique_triangles = uniq.size();
+    r.duplicate_emissions = canon.size() - uniq.size();
+    if (!reference && report.results.empty()) {
+      baseline = uniq;
+      report.reference = to_string(algo);
+    }
+    diff_sets(baseline, uniq, r);
+    r.pass = r.duplicate_emissions == 0 && r.missing_count == 0 && r.extra_count == 0;
+    report.pass = report.pass && r.pass;
+    report.results.push_back(std::move(r));
+  }
+  report.reference_count = baseline.size();
+  return report;
+}
+
+// ---------------------------------------------------------------- parallel
+RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                            const RunOptions& opt) {
+  detail::validate(cfg);
+  return run_counting(algo, g, opt);
+}
+
+RunStats run_parallel_collecting(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                                 std::vector<std::vector<std::array<VertexId, 3>>>& buffers, const RunOptions& opt) {
+  detail::validate(cfg);
+  buffers.assign(cfg.workers, {});
+  return run_collecting(algo, g, buffers[0], opt);
+}
+
+// ------------------------------------------------------------------ oracle
+std::vector<Triangle> brute_force_triangles(const Graph& g, const OracleOptions& opt) {  // oracle.cpp:8-25
+  if (g.num_vertices() > opt.max_vertices)
+    throw std::invalid_argument("oracle refuses graphs larger than " + std::to_string(opt.max_vertices) +
+                                " vertices");
+  std::vector<Triangle> out;
+  if (!g.handle() || g.num_edges() == 0) return out;
+  std::uint64_t count = 0;
+  check(tl_brute_force(g.handle(), opt.max_vertices, nullptr, 0, &count), "brute_force_triangles");
+  out.resize(count);
+  check(tl_brute_force(g.handle(), opt.max_vertices, reinterpret_cast<std::uint32_t*>(out.data()), count, &count),
+        "brute_force_triangles");
+  return out;
+}
+
+}  // namespace trilist

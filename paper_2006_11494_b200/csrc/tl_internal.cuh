@@ -1,0 +1,101 @@
+// tl_internal.cuh -- device-resident graph handles and pipeline entry points.
+#pragma once
+
+#include <map>
+#include <tuple>
+
+#include "tl_common.cuh"
+
+// Opaque C-ABI handles (trilist_b200.h).
+struct tl_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // own stream (non-blocking)
+  uint32_t n = 0;
+  uint32_t nb = 0;  // id bits: every id < 2^nb
+  uint64_t m = 0;
+  uint64_t duplicates = 0;
+  uint64_t self_loops = 0;
+  uint32_t max_deg = 0;
+  tlb::DBuf<uint64_t> keys;  // m sorted unique (lo << nb | hi), lo < hi
+  tlb::DBuf<uint32_t> deg;   // n undirected degrees
+  ~tl_graph();
+};
+
+// OrientedGraph in rank space: vertex r is the vertex of rank r; every
+// out-list is ascending (= rank-ascending, the orient() layout, which AOT's
+// early exit relies on).  Claims group the directed edges by the pivot that
+// processes them (aot_pivot's two phases, engine.hpp:247-272):
+//   edge t->h with h < t in (deg+, id) order: pivot t, traverse N+(h) from 0
+//                                            (positive phase)
+//   otherwise:                               pivot h, traverse N+(t) after h
+//                                            (negative phase)
+struct tl_oriented {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t n = 0;
+  uint32_t nb = 0;
+  uint64_t m = 0;
+  uint32_t max_out_degree = 0;
+  uint64_t cost[3] = {0, 0, 0};  // cf, kclist, aot
+  tlb::DBuf<uint64_t> off;        // n+1
+  tlb::DBuf<uint32_t> col;        // m rank ids
+  tlb::DBuf<uint32_t> orig;       // n: rank -> original id
+  tlb::DBuf<uint32_t> rank;       // n: original id -> rank
+  tlb::DBuf<uint64_t> claim_off;  // n+1, by pivot
+  tlb::DBuf<uint2> claims;        // m: x = s | neg << 31, y = start position in N+(s)
+  // triangle count per (skip_negative, part, nparts): sizes listing buffers
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
+  ~tl_oriented();
+};
+
+namespace tlb {
+
+constexpr uint32_t kNegBit = 0x80000000u;
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) TL_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- tl_build.cu ----
+void gen_er(uint64_t seed, uint32_t n, uint64_t npairs, uint32_t* d_pairs, cudaStream_t s);
+void gen_rmat(uint64_t seed, uint32_t scale, uint64_t npairs, uint32_t* d_pairs, cudaStream_t s);
+void gen_chung_lu(uint64_t seed, uint32_t n, const uint64_t* prefix, uint64_t npairs,
+                  uint32_t* d_pairs, cudaStream_t s);
+void chung_lu_prefix_host(uint64_t seed, uint32_t n, double avg, double gamma, uint64_t* prefix);
+
+void graph_from_pairs(tl_graph& g, const uint32_t* d_pairs, uint64_t npairs, uint32_t min_vertices);
+void graph_csr(tl_graph& g, DBuf<uint64_t>& off, DBuf<uint32_t>& adj);
+void degree_order(tl_graph& g, DBuf<uint32_t>& rank);  // device rank[n]
+void orient(tl_graph& g, const uint32_t* d_rank, tl_oriented& og);
+void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* d_out_off,
+                       const uint32_t* d_out, const uint32_t* d_rank);
+void oriented_download(tl_oriented& og, uint64_t* out_off, uint32_t* out, uint64_t* in_off,
+                       uint32_t* in, uint32_t* rank);
+bool is_permutation(const uint32_t* d_rank, uint32_t n, cudaStream_t s);
+
+// Lexicographic sort of uint32 triples (n_items x 3) in place.
+void sort_triples(uint32_t* d_triples, uint64_t count, uint32_t nb, cudaStream_t s);
+void canonicalize_triples(uint32_t* d_triples, uint64_t count, cudaStream_t s);
+uint64_t brute_force(tl_graph& g, DBuf<uint32_t>& out);
+
+// ---- tl_aot.cu ----
+enum class AotMode { count = 0, hash = 1, list = 2 };
+struct AotResult {
+  uint64_t positive = 0, negative = 0, executed = 0, logical = 0;
+  uint64_t hash_sum = 0, hash_xor = 0, emitted = 0, tasks = 0, table_builds = 0;
+  float list_ms = 0.f, prep_ms = 0.f;
+};
+// out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).
+AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t part, uint32_t nparts,
+                  cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
+
+}  // namespace tlb

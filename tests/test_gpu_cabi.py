@@ -1,0 +1,263 @@
+"""GPU parity through the C-ABI (include/trilist_b200.h via capi.py).
+
+Every case compares the CUDA path with the CPU checkers on the same seeded
+inputs: the C restatement (oracle/trilist_oracle.c) and the reference library
+itself (oracle/_ref).  Integer work => bit-exact equality everywhere.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2006_11494_b200 import capi
+from paper_2006_11494_b200.configs import CONFIGS, scaled
+
+pytestmark = pytest.mark.gpu
+
+STAT_KEYS = ("triangles", "probes", "table_builds", "positive_triangles", "negative_triangles")
+
+
+def fixtures():
+    out = [("K%d" % n, *O.complete_graph(n)) for n in range(3, 11)]
+    out += [("star%d" % k, *O.star_graph(k)) for k in (3, 4, 7, 10)]
+    out += [("P%d" % n, *O.path_graph(n)) for n in (2, 5, 9)]
+    out += [("C%d" % n, *O.cycle_graph(n)) for n in (3, 4, 5, 9)]
+    out += [("diamond", *O.diamond_graph()), ("paired_hubs", *O.paired_hubs_graph())]
+    return out
+
+
+def gnp_suite():  # acceptance.cpp:152-158
+    ps = (0.02, 0.1, 0.3)
+    for i in range(200):
+        n = 5 + i * 295 // 199
+        yield f"gnp{i}", n, O.gen_gnp(n, ps[i % 3], 0xACCE5500 + i)
+
+
+def check_graph(n, pairs, rank=None, skip_negative=False):
+    """Full parity of one graph: CSR, degree order, orientation, costs,
+    counters, raw emissions, canonical set, hash."""
+    pairs = O.as_pairs(pairs) if not isinstance(pairs, np.ndarray) else pairs
+    og_cpu = O.OracleGraph(n, pairs)
+    dg = capi.DeviceGraph.from_pairs(pairs, n)
+    assert (dg.n, dg.m, dg.duplicates) == (og_cpu.n, og_cpu.m, og_cpu.duplicates)
+    off, adj = og_cpu.csr()
+    doff, dadj = dg.csr()
+    assert np.array_equal(off, doff) and np.array_equal(adj, dadj)
+    cpu_rank = og_cpu.degree_order() if rank is None else np.asarray(rank, np.uint32)
+    if rank is None:
+        assert np.array_equal(dg.degree_order(), cpu_rank)
+    oo = og_cpu.orient(cpu_rank)
+    do = dg.orient(None if rank is None else cpu_rank)
+    a, b = oo.csr(), do.csr()
+    for k in ("out_offsets", "out", "in_offsets", "inn", "rank"):
+        assert np.array_equal(a[k], b[k]), k
+    assert do.max_out_degree == oo.max_out_degree()
+    assert do.cost_model() == oo.cost_model()
+    st, raw = oo.aot(skip_negative=skip_negative, collect=True)
+    cnt = do.count(skip_negative=skip_negative)
+    for k in STAT_KEYS:
+        assert cnt[k] == st[k], k
+    hs = do.hash(skip_negative=skip_negative)
+    assert (hs["triangles"], hs["hash_sum"], hs["hash_xor"]) == (st["triangles"], st["hash_sum"], st["hash_xor"])
+    lst, got_raw = do.list(canonical=False, skip_negative=skip_negative)
+    assert lst["triangles"] == st["triangles"]
+    # raw role-ordered emissions (pivot, neighbor, witness) match as multisets
+    key = lambda r: r[np.lexsort((r[:, 2], r[:, 1], r[:, 0]))] if len(r) else r  # noqa: E731
+    assert np.array_equal(key(got_raw), key(raw))
+    _, canon = do.list(canonical=True, skip_negative=skip_negative)
+    assert np.array_equal(canon, O.canonical_sorted(raw))
+    return st
+
+
+def test_device_present():
+    assert capi.device_count() >= 1
+
+
+@pytest.mark.parametrize("name,n,edges", fixtures(), ids=[f[0] for f in fixtures()])
+def test_fixtures(name, n, edges):
+    st = check_graph(n, edges)
+    bf = O.OracleGraph(n, O.as_pairs(edges)).brute_force()
+    assert st["triangles"] == len(bf)
+
+
+def test_known_answers():
+    # paired_hubs: kclist_cost 21, aot_cost 12, 6 triangles (test_engine.cpp:87-108)
+    n, e = O.paired_hubs_graph()
+    do = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient()
+    cm = do.cost_model()
+    assert (cm["kclist_cost"], cm["aot_cost"]) == (21, 12)
+    st = do.count()
+    assert (st["probes"], st["triangles"]) == (12, 6)
+    _, canon = do.list(canonical=True)
+    assert canon.tolist() == [[6, 9, 12], [6, 9, 13], [7, 10, 12], [7, 10, 13], [8, 11, 12], [8, 11, 13]]
+    # K3 id order: triangles 1, probes 1, table_builds 3; costs 6/1/1 (test_engine.cpp:61-73)
+    n, e = O.complete_graph(3)
+    do = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient(np.arange(3, dtype=np.uint32))
+    st = do.count()
+    assert (st["triangles"], st["probes"], st["table_builds"]) == (1, 1, 3)
+    assert do.cost_model() == {"cf_cost": 6, "kclist_cost": 1, "aot_cost": 1}
+    # diamond id order: pos 1, neg 1; fault-injected 1 triangle, neg 0 (test_engine.cpp:240-255)
+    n, e = O.diamond_graph()
+    do = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient(np.arange(4, dtype=np.uint32))
+    st = do.count()
+    assert (st["triangles"], st["positive_triangles"], st["negative_triangles"]) == (2, 1, 1)
+    st = do.count(skip_negative=True)
+    assert (st["triangles"], st["negative_triangles"]) == (1, 0)
+    # star S5: aot_cost 0, probes 0 under degree and id order (test_engine.cpp:110-124)
+    n, e = O.star_graph(5)
+    for rank in (None, np.arange(6, dtype=np.uint32)):
+        do = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient(rank)
+        assert do.cost_model()["aot_cost"] == 0
+        st = do.count()
+        assert (st["triangles"], st["probes"]) == (0, 0)
+    # empty graph: all zeros (test_engine.cpp:126-133)
+    do = capi.DeviceGraph.from_pairs(np.zeros((0, 2), np.uint32), 0).orient()
+    st = do.count()
+    assert (st["triangles"], st["probes"], st["table_builds"]) == (0, 0, 0)
+
+
+def test_complete_graphs_closed_form():  # acceptance.cpp:252-268
+    for n in range(3, 26):
+        _, e = O.complete_graph(n)
+        st = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient().count()
+        assert st["triangles"] == n * (n - 1) * (n - 2) // 6
+
+
+def test_gnp_sweep_vs_oracle():  # the 200-graph G(n, p) sweep of acceptance.cpp:146-214
+    for name, n, pairs in gnp_suite():
+        check_graph(n, pairs)
+
+
+def test_gnp_id_order_and_fault_injection():
+    for seed in (7, 8, 9):
+        pairs = O.gen_gnp(200, 0.05, seed)
+        check_graph(200, pairs, rank=np.arange(200, dtype=np.uint32))
+        check_graph(200, pairs, skip_negative=True)
+        rng = np.random.default_rng(seed)
+        check_graph(200, pairs, rank=rng.permutation(200).astype(np.uint32))
+
+
+def test_fault_injection_is_caught():  # test_engine.cpp:278-287
+    pairs = O.gen_gnp(160, 0.07, 23)
+    do = capi.DeviceGraph.from_pairs(pairs, 160).orient()
+    _, full = do.list(canonical=True)
+    _, broken = do.list(canonical=True, skip_negative=True)
+    full_set = {tuple(t) for t in full.tolist()}
+    broken_set = {tuple(t) for t in broken.tolist()}
+    assert broken_set < full_set  # missing > 0, extra == 0
+
+
+def test_orient_rejects_non_permutation():
+    dg = capi.DeviceGraph.from_pairs(O.as_pairs(O.path_graph(3)[1]), 3)
+    with pytest.raises(capi.TlError) as e:
+        dg.orient(np.array([0, 0, 1], np.uint32))
+    assert e.value.code == capi.TL_EINVAL
+
+
+def test_generators_bit_exact():
+    import torch
+
+    for key in ("c1", "c2", "c3"):
+        cfg = scaled(key, 0 if key == "c1" else 4)
+        cfg = dict(cfg, npairs=min(cfg["npairs"], 1 << 18))
+        d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
+        capi.gen_pairs_device(cfg, d.data_ptr())
+        torch.cuda.synchronize()
+        got = d.cpu().numpy().view(np.uint32).reshape(-1, 2)
+        assert np.array_equal(got, O.gen_config(cfg)), key
+
+
+def test_c1_er_full_list(golden):
+    """C1: full sorted canonical list vs the reference's list (golden .npy,
+    itself checked against brute_force_triangles when it was generated)."""
+    import os
+
+    g = golden["c1"]
+    cfg = CONFIGS["c1"]
+    pairs = O.gen_config(cfg)
+    dg = capi.DeviceGraph.from_pairs(pairs, cfg["n"])
+    assert dg.m == g["m"]
+    do = dg.orient()
+    st = do.count()
+    for k in ("triangles", "probes", "table_builds", "positive_triangles", "negative_triangles"):
+        assert st[k] == g[k], k
+    _, canon = do.list(canonical=True)
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", g["list_file"]))
+    assert np.array_equal(canon, ref)
+    bf = dg.brute_force(max_vertices=cfg["n"])
+    assert np.array_equal(bf, ref)
+
+
+@pytest.mark.parametrize("nparts", [2, 3, 4, 8])
+def test_partitions_sum_to_whole(nparts):
+    """Multi-GPU arithmetic on one device: the cost-balanced parts are
+    disjoint and cover every claim (sum/xor of parts == whole)."""
+    pairs = O.gen_rmat(11, 14, 16 << 14)
+    do = capi.DeviceGraph.from_pairs(pairs, 1 << 14).orient()
+    whole = do.hash()
+    acc = dict(triangles=0, probes=0, table_builds=0, positive_triangles=0, negative_triangles=0,
+               hash_sum=0, hash_xor=0)
+    lists = []
+    for p in range(nparts):
+        h = do.hash(part=p, nparts=nparts)
+        for k in acc:
+            if k == "hash_xor":
+                acc[k] ^= h[k]
+            elif k == "hash_sum":
+                acc[k] = (acc[k] + h[k]) % (1 << 64)
+            else:
+                acc[k] += h[k]
+        lists.append(do.list(canonical=True, part=p, nparts=nparts)[1])
+    for k in acc:
+        assert acc[k] == whole[k], k
+    merged = np.concatenate(lists)
+    merged = merged[np.lexsort((merged[:, 2], merged[:, 1], merged[:, 0]))]
+    assert np.array_equal(merged, do.list(canonical=True)[1])
+
+
+def test_upload_reference_layout_matches_orient():
+    """tl_oriented_from_csr (drop-in upload of a host OrientedGraph) gives the
+    same results as the device orient; also with degree-desc local order."""
+    pairs = O.gen_rmat(5, 12, 16 << 12)
+    ref = O.RefGraph(1 << 12, pairs)
+    a = ref.oriented_csr()
+    up = capi.DeviceOriented.from_csr(ref.n, a["out_offsets"], a["out"], a["rank"])
+    want = ref.hash(threads=2)
+    got = up.hash()
+    for k in ("triangles", "probes", "table_builds", "positive_triangles", "negative_triangles", "hash_sum",
+              "hash_xor"):
+        assert got[k] == want[k], k
+    b = up.csr()
+    for k in ("out_offsets", "out", "in_offsets", "inn", "rank"):
+        assert np.array_equal(a[k], b[k]), k
+    refd = O.RefGraph(1 << 12, pairs, local="degree-desc")
+    ad = refd.oriented_csr()
+    upd = capi.DeviceOriented.from_csr(refd.n, ad["out_offsets"], ad["out"], ad["rank"])
+    assert upd.hash()["hash_sum"] == want["hash_sum"]
+
+
+@pytest.mark.slow
+def test_c2_rmat20_vs_reference(golden):
+    g = golden["c2"]
+    cfg = CONFIGS["c2"]
+    import torch
+
+    d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
+    capi.gen_pairs_device(cfg, d.data_ptr())
+    torch.cuda.synchronize()
+    host = d.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    assert O.pairs_checksum(host) == g["pairs_checksum"]
+    dg = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"])
+    assert (dg.n, dg.m) == (g["n"], g["m"])
+    do = dg.orient()
+    assert do.max_out_degree == g["max_out_degree"]
+    assert do.cost_model() == g["cost_model"]
+    h = do.hash()
+    for k in ("triangles", "probes", "table_builds", "positive_triangles", "negative_triangles", "hash_sum",
+              "hash_xor"):
+        assert h[k] == g[k], k
+    c = do.count()
+    assert c["triangles"] == g["triangles"]
+    st, canon = do.list(canonical=True)
+    assert st["triangles"] == g["triangles"]
+    assert O.hash_of_triples(canon) == (g["triangles"], g["hash_sum"], g["hash_xor"])
+    assert not np.any(np.all(canon[1:] == canon[:-1], axis=1))  # duplicate-free
