@@ -51,6 +51,7 @@ typedef struct tl_stats {
   uint64_t tasks;             /* work items scheduled                                              */
   double list_ms;             /* device time of the listing kernels (CUDA events)                  */
   double prep_ms;             /* device time of per-run task construction                          */
+  uint64_t kernel_launches;   /* device kernels this call launched (task building + listing)       */
 } tl_stats;
 
 /* RunOptions (engine.hpp:56-60) + ParallelConfig-equivalent partitioning. */

@@ -33,7 +33,7 @@ class TlStats(C.Structure):
         ("triangles", C.c_uint64), ("probes", C.c_uint64), ("merge_comparisons", C.c_uint64),
         ("table_builds", C.c_uint64), ("positive_triangles", C.c_uint64), ("negative_triangles", C.c_uint64),
         ("probes_executed", C.c_uint64), ("hash_sum", C.c_uint64), ("hash_xor", C.c_uint64),
-        ("tasks", C.c_uint64), ("list_ms", C.c_double), ("prep_ms", C.c_double),
+        ("tasks", C.c_uint64), ("list_ms", C.c_double), ("prep_ms", C.c_double), ("kernel_launches", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

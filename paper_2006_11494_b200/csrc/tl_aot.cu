@@ -555,7 +555,8 @@ int sm_count() {
 }
 
 template <AotMode MODE>
-void launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
+uint64_t launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
+  uint64_t launches = 0;
   const size_t warp_smem = sizeof(uint32_t) * (kWarpsPerCta * kWarpSlots +
                                                (MODE == AotMode::list ? kWarpsPerCta * 3 * kEmitCap : 0));
   const size_t cta_smem = sizeof(uint32_t) * ((1u << kCtaSlotsLg) +
@@ -571,6 +572,7 @@ void launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
     unsigned grid = unsigned(std::min<uint64_t>(pc.ntasks, uint64_t(sms)));
     k_aot_cta<MODE><<<grid, kCtaThreads, cta_smem, s>>>(pc);
     TL_CUDA(cudaGetLastError());
+    ++launches;
   }
   if (pw.ntasks) {
     int per_sm = 0;
@@ -580,7 +582,9 @@ void launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
     unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sms) * per_sm));
     k_aot_warp<MODE><<<grid, kWarpThreads, warp_smem, s>>>(pw);
     TL_CUDA(cudaGetLastError());
+    ++launches;
   }
+  return launches;
 }
 
 }  // namespace
@@ -613,6 +617,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.claims.p, og.off.p, m, skip_negative, CP.p);
   TL_CUDA(cudaGetLastError());
   cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, CP.p, m + 1, s); });
+  r.launches += 1 + 2 + 1;  // k_claim_cost, scan (init + sweep), k_split
 
   DBuf<uint64_t> split;
   split.alloc(6, s);
@@ -634,6 +639,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claims.p, og.off.p, cb, ce, skip_negative,
                                                                acc.p + kLogical);
     TL_CUDA(cudaGetLastError());
+    ++r.launches;
   }
 
   const uint32_t np = cb < ce ? pe - pb : 0;
@@ -674,6 +680,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
                                                              ctasks.p);
     if (G) k_groups<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(SP.p, np, pb, G, cb, ce, wtasks.p + nw_chunks);
     TL_CUDA(cudaGetLastError());
+    r.launches += 1 + 3 * 2 + (nw_chunks ? 1 : 0) + (nc_chunks ? 1 : 0) + (G ? 1 : 0);
   }
   TL_CUDA(cudaEventRecord(ev[1], s));
 
@@ -695,9 +702,9 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   pc.tasks = ctasks.p;
   pc.ntasks = nc_chunks;
   switch (mode) {
-    case AotMode::count: launch_kernels<AotMode::count>(pw, pc, s); break;
-    case AotMode::hash: launch_kernels<AotMode::hash>(pw, pc, s); break;
-    case AotMode::list: launch_kernels<AotMode::list>(pw, pc, s); break;
+    case AotMode::count: r.launches += launch_kernels<AotMode::count>(pw, pc, s); break;
+    case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(pw, pc, s); break;
+    case AotMode::list: r.launches += launch_kernels<AotMode::list>(pw, pc, s); break;
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];

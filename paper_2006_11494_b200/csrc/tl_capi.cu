@@ -62,6 +62,7 @@ void fill_stats(tl_stats* st, const tlb::AotResult& r) {
   st->tasks = r.tasks;
   st->list_ms = r.list_ms;
   st->prep_ms = r.prep_ms;
+  st->kernel_launches = r.launches;
 }
 
 tl_run_options defaults() {

@@ -91,7 +91,7 @@ uint64_t brute_force(tl_graph& g, DBuf<uint32_t>& out);
 enum class AotMode { count = 0, hash = 1, list = 2 };
 struct AotResult {
   uint64_t positive = 0, negative = 0, executed = 0, logical = 0;
-  uint64_t hash_sum = 0, hash_xor = 0, emitted = 0, tasks = 0, table_builds = 0;
+  uint64_t hash_sum = 0, hash_xor = 0, emitted = 0, tasks = 0, table_builds = 0, launches = 0;
   float list_ms = 0.f, prep_ms = 0.f;
 };
 // out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).

@@ -1,0 +1,42 @@
+"""Minimal profiling driver: build + orient one config on cuda:0, then run
+`--reps` AOT calls in the given mode (for ncu: the last launches are the
+steady-state ones)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    from paper_2006_11494_b200 import capi
+    from paper_2006_11494_b200.configs import CONFIGS
+
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c2")
+    p.add_argument("--mode", default="count", choices=["count", "hash", "list"])
+    p.add_argument("--reps", type=int, default=3)
+    a = p.parse_args()
+    cfg = CONFIGS[a.config]
+    d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
+    capi.gen_pairs_device(cfg, d.data_ptr())
+    torch.cuda.synchronize()
+    og = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"]).orient()
+    del d
+    for _ in range(a.reps):
+        if a.mode == "count":
+            st = og.count()
+        elif a.mode == "hash":
+            st = og.hash()
+        else:
+            s = capi.TlStats()
+            o = capi.run_options()
+            capi._check(capi.lib().tl_aot_list(og._h, capi.C.byref(o), None, 0, 0, capi.C.byref(s)))
+            st = s.as_dict()
+    print({k: st[k] for k in ("triangles", "probes", "probes_executed", "tasks", "list_ms", "prep_ms")})
+
+
+if __name__ == "__main__":
+    main()
