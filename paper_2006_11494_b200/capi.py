@@ -14,7 +14,7 @@ from functools import lru_cache
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libtrilist_b200.so")
+LIB_PATH = os.environ.get("TL_LIB_PATH") or os.path.join(PKG, "lib", "libtrilist_b200.so")
 
 TL_OK, TL_EINVAL, TL_ERANGE, TL_ELOGIC, TL_ECUDA, TL_ENOMEM, TL_ECAPACITY, TL_ENODEV = range(8)
 

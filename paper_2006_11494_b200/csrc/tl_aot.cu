@@ -9,17 +9,23 @@
 //     traversed vertex s, the phase (positive/negative) and the first useful
 //     position in N+(s) (after l for the negative phase: a witness must rank
 //     above l);
-//   * N+(l) is staged ONCE per work item in shared memory as an open-addressing
-//     hash table (the paper's H) -- per warp for
-//     deg+(l) <= 1024, per CTA (up to 32K slots) for larger pivots, and a
+//   * N+(l) is staged ONCE per work record in shared memory.  Vertices are
+//     relabelled by rank, so N+(l) lies in [min, max] of its own ranks; when
+//     that span fits, the probe side is a direct bitmap over the span (the
+//     reference's bitmap, restricted to the window: one LDS + bit test per
+//     probe, no collision loop).  Wider spans fall back to an open-addressing
+//     hash (key + 1 stored, 0 = empty, so both layouts share the all-zero
+//     resting state).  Per warp: 8 KB (65,536-bit span or 2,048 slots); heavy
+//     pivots (deg+ > 1024 with a wide span) use a 128 KB per-CTA region, and a
 //     binary search over the sorted global list beyond that;
-//   * traversal lists are streamed with coalesced loads: lists longer than 64
-//     are swept by the whole warp (early exit as soon as a rank exceeds
-//     max N+(l), the list being rank-ascending), shorter ones are packed 32
-//     probes per round by a warp-level load-balanced search;
-//   * work items ("tasks") are cost-balanced: small pivots are grouped to
-//     ~kTaskWarp probes, heavy pivots are split into chunks of their claim
-//     list by the claim-cost prefix (the same prefix cuts multi-GPU parts).
+//   * traversal lists are streamed with coalesced loads: lists longer than 32
+//     are swept by the whole warp (4 rounds in flight, early exit once a rank
+//     exceeds max N+(l) -- lists are rank-ascending), shorter ones are packed
+//     32 probes per round by a warp-level load-balanced search;
+//   * work is described by compact records (one per pivot with work, or per
+//     chunk of a heavy pivot's claim list cut at the claim-cost prefix) and
+//     cost-balanced tasks over consecutive records, fetched dynamically; the
+//     same cost prefix cuts the multi-GPU parts.
 #include <cub/cub.cuh>
 
 #include "tl_internal.cuh"
@@ -29,29 +35,46 @@ namespace tlb {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr uint32_t kChunkBit = 0x80000000u;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range load
 
+// Tuning knobs (compile-time; see tools/sweep.py):
+#ifndef TL_UNROLL
+#define TL_UNROLL 4  // rounds of 32 traversal loads in flight per warp
+#endif
+#ifndef TL_WARP_WORDS
+#define TL_WARP_WORDS 1536  // per-warp probe region in 32-bit words (6 KB)
+#endif
+#ifndef TL_CTAS_PER_SM
+#define TL_CTAS_PER_SM 4
+#endif
+constexpr int kUnroll = TL_UNROLL;
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
 constexpr int kWarpsPerCta = kWarpThreads / 32;
-constexpr int kWarpSlotsLg = 11;  // 2048-slot table per warp (8 KB)
-constexpr int kWarpSlots = 1 << kWarpSlotsLg;
-constexpr uint32_t kWarpDegMax = kWarpSlots / 2;
+constexpr uint32_t kWarpWords = TL_WARP_WORDS;
+constexpr uint32_t kWarpWordsLg = 31 - __builtin_clz(TL_WARP_WORDS);  // largest hash table: 2^lg <= words
+constexpr uint32_t kWarpSpanMax = kWarpWords * 32;                    // bitmap span
+constexpr uint32_t kWarpHashDegMax = (1u << kWarpWordsLg) / 2;
+constexpr uint32_t kWarpStride = kWarpWords + 32;    // + an always-zero guard word (128 B aligned)
 constexpr int kCtaThreads = 512;
 constexpr int kCtaWarps = kCtaThreads / 32;
-constexpr int kCtaSlotsLg = 15;  // 32K slots (128 KB)
-constexpr uint32_t kCtaDegMax = (1u << kCtaSlotsLg) / 2;
-constexpr int kEmitCap = 64;      // per-warp staging of listed triangles
-constexpr uint32_t kLong = 64;    // claims longer than this are warp-swept
+constexpr uint32_t kCtaWordsLg = 15;
+constexpr uint32_t kCtaWords = 1u << kCtaWordsLg;  // 128 KB per CTA
+constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
+constexpr uint32_t kCtaHashDegMax = kCtaWords / 2;
+constexpr uint32_t kCtaStride = kCtaWords + 32;
+constexpr int kEmitCap = 64;     // per-warp staging of listed triangles
+constexpr uint32_t kShort = 32;  // claims of at most this length are packed
 constexpr uint64_t kTaskWarp = 4096;
 constexpr uint64_t kTaskCta = 65536;
-constexpr uint64_t kBeta = 4;     // hash build weight per N+(l) element
-constexpr uint64_t kGamma = 32;   // per-pivot overhead
-constexpr uint64_t kKappa = 2;    // per-claim overhead for the multi-GPU cut
+constexpr uint64_t kBeta = 2;    // staging weight per N+(l) element
+constexpr uint64_t kGamma = 64;  // per-record overhead
+constexpr uint64_t kKappa = 8;   // per-claim overhead (scheduling and the multi-GPU cut)
 
-struct Task {
-  uint32_t pb, pe;  // pivots [pb, pe); pe | kChunkBit = chunk of one heavy pivot
-  uint64_t cb, ce;  // claims clipped to [cb, ce)
+// One unit of work: the claims [cb, ce) of pivot l, whose out-list is
+// col[lb, lb + dl).
+struct Rec {
+  uint64_t lb, cb, ce;
+  uint32_t l, dl;
 };
 
 enum Acc : int { kPos = 0, kNeg, kExec, kHsum, kHxor, kEmitted, kWarpCounter, kCtaCounter, kLogical, kAccN };
@@ -59,18 +82,18 @@ enum Acc : int { kPos = 0, kNeg, kExec, kHsum, kHxor, kEmitted, kWarpCounter, kC
 struct Params {
   const uint64_t* off;
   const uint32_t* col;
-  const uint64_t* claim_off;
   const uint2* claims;
   const uint32_t* orig;
-  const uint8_t* pskip;  // pivots [pbase, ...): 1 = not processed by group tasks
-  uint32_t pbase;
-  uint32_t skip_neg;
-  const Task* tasks;
+  const Rec* recs;
+  const uint2* tasks;  // warp kernel: [rb, re) record ranges
   uint64_t ntasks;
+  uint32_t skip_neg;
   unsigned long long* acc;
   uint32_t* out;
   uint64_t out_cap;
 };
+
+extern __shared__ uint32_t dsmem[];  // dynamic shared memory, addressed by word offset
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -78,62 +101,112 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-
 __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
 
+// Shared memory is addressed with 32-bit shared::cta byte addresses through
+// PTX, so the hot loops never rebuild a generic/cluster-window address.
+__device__ __forceinline__ uint32_t sm_addr(uint32_t word) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(dsmem)) + 4u * word;
+}
+__device__ __forceinline__ uint32_t ld_sm(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void st_sm(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void red_or_sm(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t cas_sm(uint32_t a, uint32_t cmp, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v));
+  return old;
+}
+
 // ------------------------------------------------------------ probe sides
-struct SmemHash {
-  const uint32_t* T;
-  uint32_t mask, shift;
-  __device__ __forceinline__ bool find(uint32_t x) const {
+struct BitmapProbe {  // bit (x - lmin) of the words at byte address `base`
+  static constexpr bool kRangeChecked = true;  // bit() itself rejects x outside [lmin, lmax]
+  uint32_t base, lmin, span;
+  // Branch-free membership as 0/1 with one LDS.  Ids outside [lmin, lmax]
+  // clamp to bit `span`, which is never set (the region keeps a zero word past
+  // the largest span).
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const {
+    const uint32_t d = min(x - lmin, span);
+    return (ld_sm(base + ((d >> 5) << 2)) >> (d & 31)) & 1u;
+  }
+  __device__ __forceinline__ bool test(uint32_t x) const { return bit(x) != 0; }
+};
+
+struct HashProbe {  // linear probing, stores x + 1, 0 = empty
+  static constexpr bool kRangeChecked = false;
+  uint32_t base, mask, shift;
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const { return test(x); }
+  __device__ __forceinline__ bool test(uint32_t x) const {
+    const uint32_t key = x + 1;
     uint32_t h = hslot(x, shift);
     while (true) {
-      uint32_t v = T[h];
-      if (v == x) return true;
-      if (v == kEmpty) return false;
+      const uint32_t v = ld_sm(base + (h << 2));
+      if (v == key) return true;
+      if (v == 0) return false;
       h = (h + 1) & mask;
     }
   }
 };
 
-struct GlobalSorted {  // pivots beyond the largest shared-memory table
+struct GlobalProbe {  // pivots beyond every shared-memory layout
+  static constexpr bool kRangeChecked = false;
   const uint32_t* list;
   uint32_t len;
-  __device__ __forceinline__ bool find(uint32_t x) const {
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const { return test(x); }
+  __device__ __forceinline__ bool test(uint32_t x) const {
     uint32_t lo = 0, hi = len;
     while (lo < hi) {
-      uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = (lo + hi) >> 1;
       if (__ldg(list + mid) < x) lo = mid + 1; else hi = mid;
     }
     return lo < len && __ldg(list + lo) == x;
   }
 };
 
-__device__ __forceinline__ void hash_insert(uint32_t* T, uint32_t mask, uint32_t shift, uint32_t x) {
+__device__ __forceinline__ void bitmap_set(uint32_t base, uint32_t lmin, uint32_t x) {
+  const uint32_t d = x - lmin;
+  red_or_sm(base + ((d >> 5) << 2), 1u << (d & 31));
+}
+__device__ __forceinline__ void bitmap_clear(uint32_t base, uint32_t lmin, uint32_t x) {
+  st_sm(base + (((x - lmin) >> 5) << 2), 0u);
+}
+__device__ __forceinline__ void hash_insert(uint32_t base, uint32_t mask, uint32_t shift, uint32_t x) {
   uint32_t h = hslot(x, shift);
-  while (atomicCAS(T + h, kEmpty, x) != kEmpty) h = (h + 1) & mask;
+  while (cas_sm(base + (h << 2), 0u, x + 1) != 0u) h = (h + 1) & mask;
 }
 
 // ------------------------------------------------------------ emission
 template <AotMode MODE>
 struct Lane {
-  unsigned long long pos = 0, neg = 0, exec = 0, hsum = 0, hxor = 0;
-  uint32_t* ebuf = nullptr;  // LIST: per-warp staging (kEmitCap triples)
-  uint32_t ecount = 0;       // warp-uniform
+  uint32_t pos = 0, neg = 0;  // per record
+  unsigned long long pos64 = 0, neg64 = 0, hsum = 0, hxor = 0;
+  uint32_t ebase = 0;   // LIST: byte address of the per-warp staging buffer
+  uint32_t ecount = 0;  // warp-uniform
+  __device__ __forceinline__ void fold() {
+    pos64 += pos;
+    neg64 += neg;
+    pos = neg = 0;
+  }
 };
 
 template <AotMode MODE>
 __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
   if constexpr (MODE == AotMode::list) {
     __syncwarp();
-    uint32_t cnt = st.ecount;
+    const uint32_t cnt = st.ecount;
     if (cnt) {
       unsigned long long base = 0;
       if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
       base = __shfl_sync(kFull, base, 0);
       for (uint32_t i = lane_id(); i < 3 * cnt; i += 32) {
-        uint64_t slot = base + i / 3;
-        if (slot < P.out_cap) P.out[3 * base + i] = st.ebuf[i];
+        if (base + i / 3 < P.out_cap) P.out[3 * base + i] = ld_sm(st.ebase + 4 * i);
       }
     }
     st.ecount = 0;
@@ -141,68 +214,57 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
   }
 }
 
-// Warp-collective: every lane calls it once per probe round.
-// Emission order (pivot, neighbor, witness) as in engine.hpp:256 / :269.
+// Warp-collective: every lane calls it once per probe round (hash/list
+// modes; counters are kept by the caller).  Emission role order (pivot,
+// neighbor, witness) as in engine.hpp:256 / :269.
 template <AotMode MODE>
-__device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, bool neg, uint32_t a_orig,
-                                     uint32_t b_orig, uint32_t w) {
-  if constexpr (MODE == AotMode::count) {
+__device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, uint32_t a_orig, uint32_t b_orig,
+                                     uint32_t w) {
+  if constexpr (MODE == AotMode::hash) {
     if (hit) {
-      if (neg) ++st.neg; else ++st.pos;
+      uint32_t x = a_orig, y = b_orig, z = __ldg(P.orig + w);
+      canon3(x, y, z);
+      const uint64_t h = tri_hash(x, y, z);
+      st.hsum += h;
+      st.hxor ^= h;
     }
-  } else {
-    uint32_t c_orig = hit ? __ldg(P.orig + w) : 0;
-    if (hit) {
-      if (neg) ++st.neg; else ++st.pos;
-    }
-    if constexpr (MODE == AotMode::hash) {
+  } else if constexpr (MODE == AotMode::list) {
+    const unsigned hm = __ballot_sync(kFull, hit);
+    if (hm) {
+      const uint32_t k = __popc(hm);
+      if (st.ecount + k > kEmitCap) flush_emits(st, P);
       if (hit) {
-        uint32_t x = a_orig, y = b_orig, z = c_orig;
-        canon3(x, y, z);
-        uint64_t h = tri_hash(x, y, z);
-        st.hsum += h;
-        st.hxor ^= h;
+        const uint32_t slot = st.ebase + 12 * (st.ecount + __popc(hm & lanemask_lt()));
+        st_sm(slot, a_orig);
+        st_sm(slot + 4, b_orig);
+        st_sm(slot + 8, __ldg(P.orig + w));
       }
-    } else {
-      unsigned hm = __ballot_sync(kFull, hit);
-      if (hm) {
-        uint32_t k = __popc(hm);
-        if (st.ecount + k > kEmitCap) flush_emits(st, P);
-        if (hit) {
-          uint32_t slot = st.ecount + __popc(hm & lanemask_lt());
-          st.ebuf[3 * slot] = a_orig;
-          st.ebuf[3 * slot + 1] = b_orig;
-          st.ebuf[3 * slot + 2] = c_orig;
-        }
-        st.ecount += k;
-      }
+      st.ecount += k;
     }
   }
 }
 
 // ------------------------------------------------------------ claim batch
-// One warp processes claims [base, min(base + 32, ce)) of pivot l against the
+// One warp processes claims [base, min(base + 32, ce)) of a pivot against the
 // staged probe side.  All 32 lanes must call it.
 template <AotMode MODE, typename Probe>
-__device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe, uint32_t lmin, uint32_t lmax,
-                                            uint32_t a_orig, uint64_t base, uint64_t ce, Lane<MODE>& st) {
+__device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe, uint32_t lmax, uint32_t a_orig,
+                                            uint64_t base, uint64_t ce, Lane<MODE>& st) {
   const uint32_t lane = lane_id();
   const uint64_t c = base + lane;
-  uint32_t sflag = 0, pos = 0;
-  uint64_t b = 0, e = 0;
+  uint32_t sflag = 0;
+  uint64_t b = 0;
+  uint32_t len = 0;
   if (c < ce) {
-    uint2 cl = P.claims[c];
+    const uint2 cl = P.claims[c];
     sflag = cl.x;
-    pos = cl.y;
-    bool neg = sflag & kNegBit;
-    if (!(P.skip_neg && neg)) {
-      uint32_t s = sflag & ~kNegBit;
-      uint64_t os = P.off[s];
-      e = P.off[s + 1];
-      b = os + pos;
+    if (!(P.skip_neg && (sflag & kNegBit))) {
+      const uint32_t s = sflag & ~kNegBit;
+      const uint64_t os = P.off[s], e = P.off[s + 1];
+      b = os + cl.y;
+      len = e > b ? uint32_t(e - b) : 0;
     }
   }
-  const uint32_t len = e > b ? uint32_t(e - b) : 0;
   const bool neg = sflag & kNegBit;
   uint32_t b_orig = 0;
   if constexpr (MODE != AotMode::count) {
@@ -210,11 +272,11 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   }
 
   // ---- short claims: 32 probes per round, load-balanced over the lanes
-  const uint32_t slen = len > kLong ? 0 : len;
+  const uint32_t slen = len > kShort ? 0 : len;
   uint32_t incl = slen;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(kFull, incl, o);
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
     if (lane >= uint32_t(o)) incl += t;
   }
   const uint32_t excl = incl - slen;
@@ -225,191 +287,225 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     uint32_t i = 0;  // owner: the largest lane i with excl_i <= q
 #pragma unroll
     for (uint32_t step = 16; step; step >>= 1) {
-      uint32_t pv = __shfl_sync(kFull, excl, i + step);
+      const uint32_t pv = __shfl_sync(kFull, excl, i + step);
       if (pv <= q) i += step;
     }
     const uint64_t obm = __shfl_sync(kFull, bm, i);
     const uint32_t oflag = __shfl_sync(kFull, sflag, i);
     uint32_t oorig = 0;
     if constexpr (MODE != AotMode::count) oorig = __shfl_sync(kFull, b_orig, i);
-    const bool act = q < total;
-    const uint32_t x = act ? __ldg(P.col + obm + q) : kEmpty;
-    const bool inwin = x <= lmax;  // kEmpty > any rank
-    st.exec += inwin;
-    const bool hit = inwin && x >= lmin && probe.find(x);
-    emit(st, P, hit, oflag & kNegBit, a_orig, oorig, x);
+    const uint32_t x = q < total ? __ldg(P.col + obm + q) : kEmpty;
+    const uint32_t hit = Probe::kRangeChecked ? probe.bit(x) : uint32_t(x <= lmax && probe.test(x));
+    if (oflag & kNegBit) st.neg += hit; else st.pos += hit;
+    if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oorig, x);
   }
 
-  // ---- long claims: the whole warp sweeps one list, rank-window early exit
-  unsigned longm = __ballot_sync(kFull, len > kLong);
+  // ---- long claims: the whole warp sweeps one list, kUnroll rounds of 32
+  // loads in flight; lists are rank-ascending, so a list is abandoned once a
+  // group reaches past max N+(l)
+  unsigned longm = __ballot_sync(kFull, len > kShort);
   while (longm) {
     const int j = __ffs(longm) - 1;
     longm &= longm - 1;
     const uint64_t bj = __shfl_sync(kFull, b, j);
-    const uint64_t ej = __shfl_sync(kFull, e, j);
+    const uint32_t lj = __shfl_sync(kFull, len, j);
     const bool nj = __shfl_sync(kFull, neg, j);
     uint32_t oj = 0;
     if constexpr (MODE != AotMode::count) oj = __shfl_sync(kFull, b_orig, j);
-    for (uint64_t p0 = bj; p0 < ej; p0 += 128) {
-      uint32_t x[4];
+    const uint32_t* p = P.col + bj + lane;
+    int rem = int(lj) - int(lane);  // this lane reads p[32k] while 32k < rem
+    uint32_t hits = 0;
+    for (uint32_t r0 = 0; r0 < lj; r0 += 32 * kUnroll) {
+      uint32_t x[kUnroll];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint64_t p = p0 + 32 * k + lane;
-        x[k] = p < ej ? __ldg(P.col + p) : kEmpty;
-      }
+      for (int k = 0; k < kUnroll; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
       bool over = false;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool inwin = x[k] <= lmax;
-        st.exec += inwin;
-        over |= !inwin;
-        const bool hit = inwin && x[k] >= lmin && probe.find(x[k]);
-        emit(st, P, hit, nj, a_orig, oj, x[k]);
+      for (int k = 0; k < kUnroll; ++k) {
+        over |= x[k] > lmax;
+        const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
+        hits += hit;
+        if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oj, x[k]);
       }
+      p += 32 * kUnroll;
+      rem -= 32 * kUnroll;
       if (__any_sync(kFull, over)) break;
     }
+    if (nj) st.neg += hits; else st.pos += hits;
   }
 }
 
 template <AotMode MODE>
 __device__ __forceinline__ void reduce_and_flush(Lane<MODE>& st, const Params& P) {
+  st.fold();
   flush_emits(st, P);
-  unsigned long long v[5] = {st.pos, st.neg, st.exec, st.hsum, st.hxor};
+  unsigned long long v[4] = {st.pos64, st.neg64, st.hsum, st.hxor};
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] += __shfl_xor_sync(kFull, v[k], o);
-    v[4] ^= __shfl_xor_sync(kFull, v[4], o);
+    for (int k = 0; k < 3; ++k) v[k] += __shfl_xor_sync(kFull, v[k], o);
+    v[3] ^= __shfl_xor_sync(kFull, v[3], o);
   }
   if (lane_id() == 0) {
     if (v[0]) atomicAdd(P.acc + kPos, v[0]);
     if (v[1]) atomicAdd(P.acc + kNeg, v[1]);
-    if (v[2]) atomicAdd(P.acc + kExec, v[2]);
-    if (v[3]) atomicAdd(P.acc + kHsum, v[3]);
-    if (v[4]) atomicXor(P.acc + kHxor, v[4]);
+    if (v[2]) atomicAdd(P.acc + kHsum, v[2]);
+    if (v[3]) atomicXor(P.acc + kHxor, v[3]);
   }
 }
 
 // ------------------------------------------------------------ warp kernel
 template <AotMode MODE>
-__global__ void __launch_bounds__(kWarpThreads, 3) k_aot_warp(Params P) {
-  extern __shared__ uint32_t smem[];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  uint32_t* T = smem + warp * kWarpSlots;
-  Lane<MODE> st;
-  if constexpr (MODE == AotMode::list) st.ebuf = smem + kWarpsPerCta * kWarpSlots + warp * (3 * kEmitCap);
+__device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint32_t wbase, Lane<MODE>& st) {
+  const uint32_t lane = lane_id();
+  const uint32_t* nl = P.col + R.lb;
+  const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
+  const uint32_t span = lmax - lmin + 1;
+  uint32_t a_orig = 0;
+  if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+  if (span <= kWarpSpanMax) {
+    for (uint32_t i = lane; i < R.dl; i += 32) bitmap_set(wbase, lmin, __ldg(nl + i));
+    __syncwarp();
+    const BitmapProbe probe{wbase, lmin, span};
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+    __syncwarp();
+    const uint32_t nwords = (span + 31) >> 5;
+    if (nwords <= max(64u, 2 * R.dl))
+      for (uint32_t i = lane; i < nwords; i += 32) st_sm(wbase + 4 * i, 0u);
+    else
+      for (uint32_t i = lane; i < R.dl; i += 32) bitmap_clear(wbase, lmin, __ldg(nl + i));
+  } else {
+    uint32_t lg = 32 - __clz(4 * R.dl - 1);
+    lg = max(5u, min(lg, kWarpWordsLg));
+    const uint32_t cap = 1u << lg;
+    for (uint32_t i = lane; i < R.dl; i += 32) hash_insert(wbase, cap - 1, 32 - lg, __ldg(nl + i));
+    __syncwarp();
+    const HashProbe probe{wbase, cap - 1, 32 - lg};
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+    __syncwarp();
+    for (uint32_t i = lane; i < cap; i += 32) st_sm(wbase + 4 * i, 0u);
+  }
+  __syncwarp();
+  st.fold();
+}
 
+template <AotMode MODE>
+__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::list ? 3 : TL_CTAS_PER_SM) k_aot_warp(Params P) {
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t wbase = sm_addr(warp * kWarpStride);
+  for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
+  __syncwarp();
+  Lane<MODE> st;
+  st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (3 * kEmitCap));
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(P.acc + kWarpCounter, 1ull);
     t = __shfl_sync(kFull, t, 0);
     if (t >= P.ntasks) break;
-    const Task tk = P.tasks[t];
-    const bool chunk = tk.pe & kChunkBit;
-    const uint32_t pe = tk.pe & ~kChunkBit;
-    for (uint32_t l = tk.pb; l < pe; ++l) {
-      if (!chunk && P.pskip[l - P.pbase]) continue;
-      const uint64_t cb = max(P.claim_off[l], tk.cb), ce = min(P.claim_off[l + 1], tk.ce);
-      const uint64_t lb = P.off[l], le = P.off[l + 1];
-      const uint32_t dl = uint32_t(le - lb);
-      if (cb >= ce || dl == 0) continue;
-      // table of 2^lg >= 4 deg+(l) slots (load <= 1/4), at most kWarpSlots
-      uint32_t lg = 32 - __clz(4 * dl - 1);
-      lg = max(5u, min(lg, uint32_t(kWarpSlotsLg)));
-      const uint32_t cap = 1u << lg;
-      __syncwarp();
-      for (uint32_t i = lane; i < cap; i += 32) T[i] = kEmpty;
-      __syncwarp();
-      for (uint32_t i = lane; i < dl; i += 32) hash_insert(T, cap - 1, 32 - lg, __ldg(P.col + lb + i));
-      const uint32_t lmin = __ldg(P.col + lb), lmax = __ldg(P.col + le - 1);
-      uint32_t a_orig = 0;
-      if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + l);
-      __syncwarp();
-      const SmemHash probe{T, cap - 1, 32 - lg};
-      for (uint64_t base = cb; base < ce; base += 32) claim_batch<MODE>(P, probe, lmin, lmax, a_orig, base, ce, st);
-    }
+    const uint2 tk = P.tasks[P.ntasks - 1 - t];  // heaviest pivots (highest ranks) first
+    for (uint32_t r = tk.x; r < tk.y; ++r) warp_record(P, P.recs[r], wbase, st);
   }
   reduce_and_flush(st, P);
 }
 
 // ------------------------------------------------------------ CTA kernel
-// Heavy pivots (deg+ > kWarpDegMax): one shared table per CTA, the CTA's
-// warps split the chunk's claims.
+// Heavy pivots (deg+ > 1024 and a span beyond the warp bitmap): one shared
+// probe side per CTA; the CTA's warps split the record's claims.
+template <AotMode MODE, typename Probe>
+__device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
+                                           uint32_t a_orig, Lane<MODE>& st) {
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint64_t base = R.cb + 32 * warp; base < R.ce; base += 32 * kCtaWarps)
+    claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+}
+
 template <AotMode MODE>
 __global__ void __launch_bounds__(kCtaThreads, 1) k_aot_cta(Params P) {
-  extern __shared__ uint32_t smem[];
   __shared__ unsigned long long s_task;
   const uint32_t warp = threadIdx.x >> 5;
-  uint32_t* T = smem;
+  const uint32_t cbase = sm_addr(0);
+  for (uint32_t i = threadIdx.x; i < kCtaStride; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
+  __syncthreads();
   Lane<MODE> st;
-  if constexpr (MODE == AotMode::list) st.ebuf = smem + (1u << kCtaSlotsLg) + warp * (3 * kEmitCap);
-
+  st.ebase = sm_addr(kCtaStride + warp * (3 * kEmitCap));
   while (true) {
     if (threadIdx.x == 0) s_task = atomicAdd(P.acc + kCtaCounter, 1ull);
     __syncthreads();
     const unsigned long long t = s_task;
     __syncthreads();
     if (t >= P.ntasks) break;
-    const Task tk = P.tasks[t];
-    const uint32_t l = tk.pb;
-    const uint64_t cb = tk.cb, ce = tk.ce;
-    const uint64_t lb = P.off[l], le = P.off[l + 1];
-    const uint32_t dl = uint32_t(le - lb);
-    if (cb >= ce || dl == 0) continue;
-    const uint32_t lmin = __ldg(P.col + lb), lmax = __ldg(P.col + le - 1);
+    const Rec R = P.recs[t];
+    const uint32_t* nl = P.col + R.lb;
+    const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
+    const uint32_t span = lmax - lmin + 1;
     uint32_t a_orig = 0;
-    if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + l);
-    if (dl <= kCtaDegMax) {
-      uint32_t lg = 32 - __clz(2 * dl - 1);
-      lg = max(5u, min(lg, uint32_t(kCtaSlotsLg)));
+    if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+    if (span <= kCtaSpanMax) {
+      for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) bitmap_set(cbase, lmin, __ldg(nl + i));
+      __syncthreads();
+      cta_claims(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
+      __syncthreads();
+      const uint32_t nwords = (span + 31) >> 5;
+      if (nwords <= max(uint32_t(kCtaThreads), 2 * R.dl))
+        for (uint32_t i = threadIdx.x; i < nwords; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
+      else
+        for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) bitmap_clear(cbase, lmin, __ldg(nl + i));
+    } else if (R.dl <= kCtaHashDegMax) {
+      uint32_t lg = 32 - __clz(2 * R.dl - 1);
+      lg = max(5u, min(lg, kCtaWordsLg));
       const uint32_t cap = 1u << lg;
-      for (uint32_t i = threadIdx.x; i < cap; i += kCtaThreads) T[i] = kEmpty;
+      for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < dl; i += kCtaThreads) hash_insert(T, cap - 1, 32 - lg, __ldg(P.col + lb + i));
+      cta_claims(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
       __syncthreads();
-      const SmemHash probe{T, cap - 1, 32 - lg};
-      for (uint64_t base = cb + 32 * warp; base < ce; base += 32 * kCtaWarps)
-        claim_batch<MODE>(P, probe, lmin, lmax, a_orig, base, ce, st);
+      for (uint32_t i = threadIdx.x; i < cap; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
     } else {
-      const GlobalSorted probe{P.col + lb, dl};
-      for (uint64_t base = cb + 32 * warp; base < ce; base += 32 * kCtaWarps)
-        claim_batch<MODE>(P, probe, lmin, lmax, a_orig, base, ce, st);
+      cta_claims(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
     }
+    st.fold();
     __syncthreads();
   }
   reduce_and_flush(st, P);
 }
 
-// ------------------------------------------------------------ task building
+// ------------------------------------------------------------ work building
 #define TL_GRID_STRIDE(i, count) \
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (count); i += uint64_t(gridDim.x) * blockDim.x)
 
-// Claim cost (window upper bound): deg+(s) - pos; 0 for skipped negative claims.
-__global__ void k_claim_cost(const uint2* claims, const uint64_t* off, uint64_t m, uint32_t skip_neg, uint64_t* cost) {
+// Claim cost (window upper bound): deg+(s) - pos; 0 for skipped negative
+// claims.  With `logical`, also sums the logical probes (deg+(s) per claim).
+__global__ void k_claim_cost(const uint2* claims, const uint64_t* off, uint64_t m, uint32_t skip_neg, uint64_t* cost,
+                             unsigned long long* logical) {
+  unsigned long long lsum = 0;
   TL_GRID_STRIDE(i, m + 1) {
     uint64_t c = 0;
     if (i < m) {
-      uint2 cl = claims[i];
-      bool neg = cl.x & kNegBit;
-      if (!(skip_neg && neg)) {
-        uint32_t s = cl.x & ~kNegBit;
-        c = (off[s + 1] - off[s]) - cl.y;
+      const uint2 cl = claims[i];
+      if (!(skip_neg && (cl.x & kNegBit))) {
+        const uint32_t s = cl.x & ~kNegBit;
+        const uint64_t d = off[s + 1] - off[s];
+        c = d - cl.y;
+        lsum += d;
       }
     }
     cost[i] = c;
+  }
+  if (logical) {
+    for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+    if ((threadIdx.x & 31) == 0 && lsum) atomicAdd(logical, lsum);
   }
 }
 
 __device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t lo, uint64_t hi, uint64_t x) {
   while (lo < hi) {
-    uint64_t mid = lo + (hi - lo) / 2;
+    const uint64_t mid = lo + (hi - lo) / 2;
     if (a[mid] < x) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t lo, uint64_t hi, uint64_t x) {
   while (lo < hi) {
-    uint64_t mid = lo + (hi - lo) / 2;
+    const uint64_t mid = lo + (hi - lo) / 2;
     if (a[mid] <= x) lo = mid + 1; else hi = mid;
   }
   return lo;
@@ -418,19 +514,19 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t 
 // Cost-balanced cut of the claim index space: part p owns claims
 // [cut(p), cut(p+1)), cut(k) = first i with CP[i] + kKappa*i >= k*Total/nparts.
 // out: cb, ce, pb (pivot of cb), pe (one past the pivot of ce-1),
-//      vb, ve (pivot attribution range for table_builds).
-__global__ void k_split(const uint64_t* CP, uint64_t m, const uint64_t* claim_off, uint32_t n, uint32_t part,
-                        uint32_t nparts, uint64_t* out) {
+//      vb, ve (pivot range attributed to this part), table_builds.
+__global__ void k_split(const uint64_t* CP, uint64_t m, const uint64_t* claim_off, const uint64_t* off, uint32_t n,
+                        uint32_t part, uint32_t nparts, uint64_t* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const unsigned __int128 total = (unsigned __int128)CP[m] + (unsigned __int128)kKappa * m;
   auto cut = [&](uint32_t k) -> uint64_t {
     if (k == 0) return 0;
     if (k >= nparts) return m;
-    unsigned __int128 target = total * k / nparts;
+    const unsigned __int128 target = total * k / nparts;
     uint64_t lo = 0, hi = m;
     while (lo < hi) {
-      uint64_t mid = lo + (hi - lo) / 2;
-      unsigned __int128 v = (unsigned __int128)CP[mid] + (unsigned __int128)kKappa * mid;
+      const uint64_t mid = lo + (hi - lo) / 2;
+      const unsigned __int128 v = (unsigned __int128)CP[mid] + (unsigned __int128)kKappa * mid;
       if (v < target) lo = mid + 1; else hi = mid;
     }
     return lo;
@@ -445,17 +541,18 @@ __global__ void k_split(const uint64_t* CP, uint64_t m, const uint64_t* claim_of
   out[3] = cb < ce ? pivot_of(ce - 1) + 1 : 0;
   out[4] = part == 0 ? 0 : (cb < m ? pivot_of(cb) : n);
   out[5] = part + 1 >= nparts ? n : (ce < m ? pivot_of(ce) : n);
+  out[6] = off[out[5]] - off[out[4]];  // table_builds: sum of deg+ over the attributed pivots
 }
 
-// Logical probes (engine.hpp:250/:264: one per traversed element of the full
+// Logical probes (engine.hpp:250/:264: one per element of the full traversed
 // list) over the part's claims.
 __global__ void k_logical(const uint2* claims, const uint64_t* off, uint64_t cb, uint64_t ce, uint32_t skip_neg,
                           unsigned long long* acc) {
   unsigned long long sum = 0;
   TL_GRID_STRIDE(k, ce - cb) {
-    uint2 cl = claims[cb + k];
+    const uint2 cl = claims[cb + k];
     if (!(skip_neg && (cl.x & kNegBit))) {
-      uint32_t s = cl.x & ~kNegBit;
+      const uint32_t s = cl.x & ~kNegBit;
       sum += off[s + 1] - off[s];
     }
   }
@@ -463,74 +560,75 @@ __global__ void k_logical(const uint2* claims, const uint64_t* off, uint64_t cb,
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
 }
 
-struct PivotClass {
-  uint8_t* skip;
-  uint64_t* sw;   // small-pivot weight (grouped)
-  uint32_t* nchw; // chunks for the warp kernel
-  uint32_t* nchc; // chunks for the CTA kernel
-};
+__device__ __forceinline__ bool warp_path(uint32_t dl, uint32_t span) {
+  return span <= kWarpSpanMax || dl <= kWarpHashDegMax;
+}
 
-__global__ void k_classify(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, uint32_t pb, uint32_t np,
-                           uint64_t cb, uint64_t ce, PivotClass pc) {
+// Per pivot of the part: number of warp records / CTA records.
+__global__ void k_classify(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, const uint32_t* col,
+                           uint32_t pb, uint32_t np, uint64_t cb, uint64_t ce, uint32_t* nrw, uint32_t* nrc) {
   TL_GRID_STRIDE(i, uint64_t(np) + 1) {
-    if (i == np) {
-      pc.sw[i] = 0;
-      pc.nchw[i] = 0;
-      pc.nchc[i] = 0;
-      continue;
-    }
-    const uint32_t l = pb + uint32_t(i);
-    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
-    const uint64_t W = a < b ? CP[b] - CP[a] : 0;
-    const uint64_t dl = off[l + 1] - off[l];
-    uint8_t skip = 1;
-    uint64_t sw = 0;
     uint32_t nw = 0, nc = 0;
-    if (W && dl) {
-      const uint64_t weight = W + kBeta * dl + kGamma;
-      if (weight <= kTaskWarp && dl <= kWarpDegMax) {
-        skip = 0;
-        sw = weight;
-      } else if (dl <= kWarpDegMax) {
-        nw = uint32_t((W + kTaskWarp - 1) / kTaskWarp);
-      } else {
-        nc = uint32_t((W + kTaskCta - 1) / kTaskCta);
+    if (i < np) {
+      const uint32_t l = pb + uint32_t(i);
+      const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
+      const uint64_t W = a < b ? CP[b] - CP[a] : 0;
+      const uint64_t Wk = W + kKappa * (b - a);  // work incl. per-claim overhead
+      const uint64_t lb = off[l];
+      const uint32_t dl = uint32_t(off[l + 1] - lb);
+      if (W && dl) {
+        const uint32_t span = col[lb + dl - 1] - col[lb] + 1;
+        if (warp_path(dl, span))
+          nw = uint32_t((Wk + kTaskWarp - 1) / kTaskWarp);
+        else
+          nc = uint32_t((Wk + kTaskCta - 1) / kTaskCta);
       }
     }
-    pc.skip[i] = skip;
-    pc.sw[i] = sw;
-    pc.nchw[i] = nw;
-    pc.nchc[i] = nc;
+    nrw[i] = nw;
+    nrc[i] = nc;
   }
 }
 
-// Chunks of heavy pivots: chunk k of pivot l covers the claims whose cost
-// prefix falls in [W*k/nch, W*(k+1)/nch).
-__global__ void k_chunks(const uint64_t* CP, const uint64_t* claim_off, uint32_t pb, uint32_t np, uint64_t cb,
-                         uint64_t ce, const uint32_t* nch, const uint32_t* nch_off, Task* tasks) {
-  TL_GRID_STRIDE(i, uint64_t(np)) {
-    const uint32_t k = nch[i];
-    if (!k) continue;
-    const uint32_t l = pb + uint32_t(i);
-    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
-    const uint64_t base = CP[a], W = CP[b] - base;
-    Task* out = tasks + nch_off[i];
-    uint64_t prev = a;
-    for (uint32_t j = 0; j < k; ++j) {
-      uint64_t next = j + 1 == k ? b : lower_bound_u64(CP, a, b, base + (W * (j + 1)) / k);
-      out[j] = Task{l, (l + 1) | kChunkBit, prev, next};
-      prev = next;
+// Record j (one thread each): pivot i = the one whose record range contains
+// j; its chunk jj covers the claims whose cost prefix falls in
+// [W*jj/k, W*(jj+1)/k).  Warp records also get their scheduling weight.
+__global__ void k_records(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, uint32_t pb, uint32_t np,
+                          uint64_t cb, uint64_t ce, const uint32_t* nr, const uint32_t* nr_off, uint64_t nrec, Rec* recs,
+                          uint64_t* weight) {
+  TL_GRID_STRIDE(j, nrec) {
+    uint32_t lo = 0, hi = np;  // largest i with nr_off[i] <= j
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (nr_off[mid] <= j) lo = mid; else hi = mid;
     }
+    const uint32_t i = lo, k = nr[i], jj = uint32_t(j - nr_off[i]);
+    const uint32_t l = pb + i;
+    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
+    // cut at the weighted prefix CP[i] + kKappa * i (monotone in i)
+    const uint64_t base = CP[a] + kKappa * a, W = CP[b] + kKappa * b - base;
+    auto cut = [&](uint64_t target) {
+      uint64_t lo = a, hi = b;
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (CP[mid] + kKappa * mid < target) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    const uint64_t from = jj == 0 ? a : cut(base + (W * jj) / k);
+    const uint64_t to = jj + 1 == k ? b : cut(base + (W * (jj + 1)) / k);
+    const uint64_t lb = off[l];
+    const uint32_t dl = uint32_t(off[l + 1] - lb);
+    recs[j] = Rec{lb, from, to, l, dl};
+    if (weight) weight[j] = (CP[to] - CP[from]) + kKappa * (to - from) + kBeta * dl + kGamma;
   }
 }
 
-// Group g = small pivots whose weight prefix SP lies in [g*T, (g+1)*T).
-__global__ void k_groups(const uint64_t* SP, uint32_t np, uint32_t pb, uint64_t G, uint64_t cb, uint64_t ce,
-                         Task* tasks) {
+// Task g = the warp records whose weight prefix RP lies in [g*T, (g+1)*T).
+__global__ void k_tasks(const uint64_t* RP, uint32_t nrec, uint64_t G, uint2* tasks) {
   TL_GRID_STRIDE(g, G) {
-    uint64_t lo = lower_bound_u64(SP, 0, np, g * kTaskWarp);
-    uint64_t hi = g + 1 == G ? np : lower_bound_u64(SP, 0, np, (g + 1) * kTaskWarp);
-    tasks[g] = Task{pb + uint32_t(lo), pb + uint32_t(hi), cb, ce};
+    const uint64_t lo = lower_bound_u64(RP, 0, nrec, g * kTaskWarp);
+    const uint64_t hi = g + 1 == G ? nrec : lower_bound_u64(RP, 0, nrec, (g + 1) * kTaskWarp);
+    tasks[g] = make_uint2(uint32_t(lo), uint32_t(hi));
   }
 }
 
@@ -544,32 +642,23 @@ void cub_call(cudaStream_t s, F&& f) {
 }
 
 int sm_count() {
-  static int cached = -1;
-  if (cached < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-    if (cached <= 0) cached = 148;
-  }
-  return cached;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
 }
 
 template <AotMode MODE>
 uint64_t launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
   uint64_t launches = 0;
-  const size_t warp_smem = sizeof(uint32_t) * (kWarpsPerCta * kWarpSlots +
-                                               (MODE == AotMode::list ? kWarpsPerCta * 3 * kEmitCap : 0));
-  const size_t cta_smem = sizeof(uint32_t) * ((1u << kCtaSlotsLg) +
-                                              (MODE == AotMode::list ? kCtaWarps * 3 * kEmitCap : 0));
-  static bool configured = false;
-  if (!configured) {
-    TL_CUDA(cudaFuncSetAttribute(k_aot_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(warp_smem)));
-    TL_CUDA(cudaFuncSetAttribute(k_aot_cta<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem)));
-    configured = true;
-  }
+  const size_t warp_smem =
+      sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE == AotMode::list ? kWarpsPerCta * 3 * kEmitCap : 0));
+  const size_t cta_smem = sizeof(uint32_t) * (kCtaStride + (MODE == AotMode::list ? kCtaWarps * 3 * kEmitCap : 0));
+  TL_CUDA(cudaFuncSetAttribute(k_aot_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(warp_smem)));
+  TL_CUDA(cudaFuncSetAttribute(k_aot_cta<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem)));
   const int sms = sm_count();
   if (pc.ntasks) {
-    unsigned grid = unsigned(std::min<uint64_t>(pc.ntasks, uint64_t(sms)));
+    const unsigned grid = unsigned(std::min<uint64_t>(pc.ntasks, uint64_t(sms)));
     k_aot_cta<MODE><<<grid, kCtaThreads, cta_smem, s>>>(pc);
     TL_CUDA(cudaGetLastError());
     ++launches;
@@ -578,8 +667,8 @@ uint64_t launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
     int per_sm = 0;
     TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot_warp<MODE>, kWarpThreads, warp_smem));
     per_sm = std::max(per_sm, 1);
-    uint64_t want = (pw.ntasks + kWarpsPerCta - 1) / kWarpsPerCta;
-    unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sms) * per_sm));
+    const uint64_t want = (pw.ntasks + kWarpsPerCta - 1) / kWarpsPerCta;
+    const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sms) * per_sm));
     k_aot_warp<MODE><<<grid, kWarpThreads, warp_smem, s>>>(pw);
     TL_CUDA(cudaGetLastError());
     ++launches;
@@ -614,93 +703,103 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   // claim-cost prefix CP[0..m]
   DBuf<uint64_t> CP;
   CP.alloc(m + 1, s);
-  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.claims.p, og.off.p, m, skip_negative, CP.p);
+  const bool whole = nparts == 1;
+  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.claims.p, og.off.p, m, skip_negative, CP.p,
+                                                               whole ? acc.p + kLogical : nullptr);
   TL_CUDA(cudaGetLastError());
   cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, CP.p, m + 1, s); });
-  r.launches += 1 + 2 + 1;  // k_claim_cost, scan (init + sweep), k_split
-
-  DBuf<uint64_t> split;
-  split.alloc(6, s);
-  k_split<<<1, 32, 0, s>>>(CP.p, m, og.claim_off.p, og.n, part, nparts, split.p);
-  TL_CUDA(cudaGetLastError());
-  uint64_t hs[6];
-  TL_CUDA(cudaMemcpyAsync(hs, split.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  TL_CUDA(cudaStreamSynchronize(s));
-  const uint64_t cb = hs[0], ce = hs[1];
-  const uint32_t pb = uint32_t(hs[2]), pe = uint32_t(hs[3]);
-  {  // table_builds attribution: sum of deg+ over pivots [vb, ve)
-    uint64_t ob = 0, oe = 0;
-    TL_CUDA(cudaMemcpyAsync(&ob, og.off.p + hs[4], 8, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaMemcpyAsync(&oe, og.off.p + hs[5], 8, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaStreamSynchronize(s));
-    r.table_builds = oe - ob;
-  }
-  if (cb < ce) {
-    k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claims.p, og.off.p, cb, ce, skip_negative,
-                                                               acc.p + kLogical);
+  r.launches += 1 + 2;  // k_claim_cost, scan (init + sweep)
+  uint64_t cb = 0, ce = m;
+  uint32_t pb = 0, pe = og.n;
+  if (whole) {
+    r.table_builds = m;
+  } else {
+    DBuf<uint64_t> split;
+    split.alloc(8, s);
+    k_split<<<1, 32, 0, s>>>(CP.p, m, og.claim_off.p, og.off.p, og.n, part, nparts, split.p);
     TL_CUDA(cudaGetLastError());
+    uint64_t hs[8];
+    TL_CUDA(cudaMemcpyAsync(hs, split.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+    cb = hs[0];
+    ce = hs[1];
+    pb = uint32_t(hs[2]);
+    pe = uint32_t(hs[3]);
+    r.table_builds = hs[6];
     ++r.launches;
+    if (cb < ce) {
+      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claims.p, og.off.p, cb, ce, skip_negative,
+                                                                 acc.p + kLogical);
+      TL_CUDA(cudaGetLastError());
+      ++r.launches;
+    }
   }
 
   const uint32_t np = cb < ce ? pe - pb : 0;
-  DBuf<uint8_t> pskip;
-  DBuf<uint64_t> SP;
-  DBuf<uint32_t> nchw, nchc, ow, oc;
-  DBuf<Task> wtasks, ctasks;
-  uint64_t nw_chunks = 0, nc_chunks = 0, G = 0;
+  DBuf<uint32_t> nrw, nrc, ow, oc;
+  DBuf<Rec> wrecs, crecs;
+  DBuf<uint64_t> wgt;
+  DBuf<uint2> tasks;
+  uint64_t nw = 0, nc = 0, G = 0;
   if (np) {
-    pskip.alloc(np + 1, s);
-    SP.alloc(np + 1, s);
-    nchw.alloc(np + 1, s);
-    nchc.alloc(np + 1, s);
+    nrw.alloc(np + 1, s);
+    nrc.alloc(np + 1, s);
     ow.alloc(np + 1, s);
     oc.alloc(np + 1, s);
-    k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, pb, np, cb,
-                                                                          ce, PivotClass{pskip.p, SP.p, nchw.p, nchc.p});
+    k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, og.col.p,
+                                                                          pb, np, cb, ce, nrw.p, nrc.p);
     TL_CUDA(cudaGetLastError());
-    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, SP.p, np + 1, s); });
-    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nchw.p, ow.p, np + 1, s); });
-    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nchc.p, oc.p, np + 1, s); });
-    uint64_t sp_total = 0;
+    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrw.p, ow.p, np + 1, s); });
+    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrc.p, oc.p, np + 1, s); });
     uint32_t tw = 0, tc = 0;
-    TL_CUDA(cudaMemcpyAsync(&sp_total, SP.p + np, 8, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaMemcpyAsync(&tw, ow.p + np, 4, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaMemcpyAsync(&tc, oc.p + np, 4, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaStreamSynchronize(s));
-    nw_chunks = tw;
-    nc_chunks = tc;
-    G = sp_total ? (sp_total - 1) / kTaskWarp + 1 : 0;
-    wtasks.alloc(std::max<uint64_t>(nw_chunks + G, 1), s);
-    ctasks.alloc(std::max<uint64_t>(nc_chunks, 1), s);
-    if (nw_chunks)
-      k_chunks<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, pb, np, cb, ce, nchw.p, ow.p,
-                                                             wtasks.p);
-    if (nc_chunks)
-      k_chunks<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, pb, np, cb, ce, nchc.p, oc.p,
-                                                             ctasks.p);
-    if (G) k_groups<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(SP.p, np, pb, G, cb, ce, wtasks.p + nw_chunks);
-    TL_CUDA(cudaGetLastError());
-    r.launches += 1 + 3 * 2 + (nw_chunks ? 1 : 0) + (nc_chunks ? 1 : 0) + (G ? 1 : 0);
+    nw = tw;
+    nc = tc;
+    r.launches += 1 + 2 * 2;
+    if (nw) {
+      wrecs.alloc(nw, s);
+      wgt.alloc(nw + 1, s);
+      TL_CUDA(cudaMemsetAsync(wgt.p + nw, 0, 8, s));
+      k_records<<<grid_for(nw, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, pb, np, cb, ce, nrw.p,
+                                                              ow.p, nw, wrecs.p, wgt.p);
+      TL_CUDA(cudaGetLastError());
+      cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, wgt.p, nw + 1, s); });
+      uint64_t total = 0;
+      TL_CUDA(cudaMemcpyAsync(&total, wgt.p + nw, 8, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+      G = total ? (total - 1) / kTaskWarp + 1 : 0;
+      tasks.alloc(std::max<uint64_t>(G, 1), s);
+      if (G) k_tasks<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(wgt.p, uint32_t(nw), G, tasks.p);
+      TL_CUDA(cudaGetLastError());
+      r.launches += 1 + 2 + (G ? 1 : 0);
+    }
+    if (nc) {
+      crecs.alloc(nc, s);
+      k_records<<<grid_for(nc, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, pb, np, cb, ce, nrc.p,
+                                                              oc.p, nc, crecs.p, nullptr);
+      TL_CUDA(cudaGetLastError());
+      ++r.launches;
+    }
   }
   TL_CUDA(cudaEventRecord(ev[1], s));
 
   Params P{};
   P.off = og.off.p;
   P.col = og.col.p;
-  P.claim_off = og.claim_off.p;
   P.claims = og.claims.p;
   P.orig = og.orig.p;
-  P.pskip = pskip.p;
-  P.pbase = pb;
   P.skip_neg = skip_negative;
   P.acc = acc.p;
   P.out = d_out;
   P.out_cap = out_cap;
   Params pw = P, pc = P;
-  pw.tasks = wtasks.p;
-  pw.ntasks = nw_chunks + G;
-  pc.tasks = ctasks.p;
-  pc.ntasks = nc_chunks;
+  pw.recs = wrecs.p;
+  pw.tasks = tasks.p;
+  pw.ntasks = G;
+  pc.recs = crecs.p;
+  pc.ntasks = nc;
   switch (mode) {
     case AotMode::count: r.launches += launch_kernels<AotMode::count>(pw, pc, s); break;
     case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(pw, pc, s); break;
@@ -708,18 +807,21 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];
+  uint64_t wcb = 0, wce = 0;
   TL_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaMemcpyAsync(&wcb, CP.p + cb, 8, cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaMemcpyAsync(&wce, CP.p + ce, 8, cudaMemcpyDeviceToHost, s));
   TL_CUDA(cudaStreamSynchronize(s));
   TL_CUDA(cudaEventElapsedTime(&r.prep_ms, ev[0], ev[1]));
   TL_CUDA(cudaEventElapsedTime(&r.list_ms, ev[1], ev[2]));
   r.positive = h[kPos];
   r.negative = h[kNeg];
-  r.executed = h[kExec];
+  r.executed = wce - wcb;  // probes left after the rank-window pruning of each list
   r.logical = h[kLogical];
   r.hash_sum = h[kHsum];
   r.hash_xor = h[kHxor];
   r.emitted = h[kEmitted];
-  r.tasks = nw_chunks + G + nc_chunks;
+  r.tasks = G + nc;
   return r;
 }
 

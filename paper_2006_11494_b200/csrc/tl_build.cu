@@ -179,13 +179,15 @@ __global__ void k_perm_check(const uint32_t* rank, uint64_t n, uint8_t* seen, ui
   }
 }
 
-// off[v] = first index e with row(e) >= v, for v in [0, n]; rows ascending.
+// Row lengths of a sorted key array (row(e) = key >> shift) from its run
+// boundaries: the first element of a run subtracts its index, the last adds
+// index + 1 -- one write per run end, no contention, rows without keys stay 0.
 template <typename K>
-__global__ void k_fill_offsets(const K* keys, uint32_t shift, uint64_t m, uint32_t n, uint64_t* off) {
-  TL_GRID_STRIDE(e, m + 1) {
-    int64_t cur = e < m ? int64_t(uint64_t(keys[e]) >> shift) : int64_t(n);
-    int64_t prev = e > 0 ? int64_t(uint64_t(keys[e - 1]) >> shift) : -1;
-    for (int64_t v = prev + 1; v <= cur; ++v) off[v] = e;
+__global__ void k_run_lengths(const K* keys, uint32_t shift, uint64_t m, unsigned long long* len) {
+  TL_GRID_STRIDE(e, m) {
+    const uint64_t row = uint64_t(keys[e]) >> shift;
+    if (e == 0 || (uint64_t(keys[e - 1]) >> shift) != row) atomicAdd(len + row, 0ull - e);
+    if (e + 1 == m || (uint64_t(keys[e + 1]) >> shift) != row) atomicAdd(len + row, e + 1);
   }
 }
 
@@ -381,6 +383,24 @@ __global__ void k_brute(const uint64_t* keys, uint64_t m, uint32_t nb, const uin
   }
 }
 
+
+// off[v] = first index e with row(e) >= v, for v in [0, n] (rows ascending):
+// run lengths from the run boundaries, then an exclusive scan.
+template <typename K>
+void fill_offsets(const K* keys, uint32_t shift, uint64_t m, uint32_t n, uint64_t* off, cudaStream_t s) {
+  DBuf<uint64_t> len;
+  len.alloc(uint64_t(n) + 1, s);
+  TL_CUDA(cudaMemsetAsync(len.p, 0, sizeof(uint64_t) * (uint64_t(n) + 1), s));
+  if (m) {
+    k_run_lengths<<<grid_for(m, kBlock, 148u * 64u), kBlock, 0, s>>>(
+        keys, shift, m, reinterpret_cast<unsigned long long*>(len.p));
+    TL_CUDA(cudaGetLastError());
+  }
+  cub_call(s, [&](void* t, size_t& bytes) {
+    return cub::DeviceScan::ExclusiveSum(t, bytes, len.p, off, uint64_t(n) + 1, s);
+  });
+}
+
 }  // namespace
 
 // ===================================================================== API
@@ -517,7 +537,7 @@ void graph_csr(tl_graph& g, DBuf<uint64_t>& off, DBuf<uint32_t>& adj) {
   k_sym_keys<<<grid_for(g.m, kBlock, 148u * 64u), kBlock, 0, s>>>(g.keys.p, g.m, g.nb, k2.p);
   TL_CUDA(cudaGetLastError());
   radix_sort_keys(k2, tmp, m2, int(2 * g.nb), s);
-  k_fill_offsets<<<grid_for(m2 + 1, kBlock, 148u * 64u), kBlock, 0, s>>>(k2.p, g.nb, m2, g.n, off.p);
+  fill_offsets(k2.p, g.nb, m2, g.n, off.p, s);
   k_low_bits<<<grid_for(m2, kBlock, 148u * 64u), kBlock, 0, s>>>(k2.p, m2, g.nb, adj.p);
   TL_CUDA(cudaGetLastError());
 }
@@ -591,8 +611,7 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   radix_sort_pairs(ckey, ckey2, dk, val2, m, int(og.nb), s);
   ckey2.reset();
   val2.reset();
-  k_fill_offsets<<<grid_for(m + 1, kBlock, 148u * 64u), kBlock, 0, s>>>(ckey.p, 0, m, og.n, og.claim_off.p);
-  TL_CUDA(cudaGetLastError());
+  fill_offsets(ckey.p, 0, m, og.n, og.claim_off.p, s);
   // claims take over the value buffer: (pos << 32 | s) == uint2{s, pos}
   og.claims.reset();
   og.claims.p = reinterpret_cast<uint2*>(dk.p);
@@ -635,8 +654,7 @@ void orient(tl_graph& g, const uint32_t* d_rank, tl_oriented& og) {
     radix_sort_keys(dk, tmp, m, int(2 * g.nb), s);
     tmp.reset();
   }
-  k_fill_offsets<<<grid_for(m + 1, kBlock, 148u * 64u), kBlock, 0, s>>>(dk.p, og.nb, m, og.n, og.off.p);
-  TL_CUDA(cudaGetLastError());
+  fill_offsets(dk.p, og.nb, m, og.n, og.off.p, s);
   finish_orient(og, dk);
 }
 
@@ -724,7 +742,7 @@ void oriented_download(tl_oriented& og, uint64_t* out_off, uint32_t* out, uint64
       radix_sort_keys(ik, tmp, m, int(2 * og.nb), s);
       tmp.reset();
     }
-    k_fill_offsets<<<grid_for(m + 1, kBlock, 148u * 64u), kBlock, 0, s>>>(ik.p, og.nb, m, og.n, roff.p);
+    fill_offsets(ik.p, og.nb, m, og.n, roff.p, s);
     deg.alloc(n + 1, s);
     doff.alloc(n + 1, s);
     k_orig_degrees<<<grid_for(n + 1, kBlock), kBlock, 0, s>>>(og.rank.p, og.n, roff.p, deg.p);

@@ -25,6 +25,7 @@ def main():
     torch.cuda.synchronize()
     og = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"]).orient()
     del d
+    best = None
     for _ in range(a.reps):
         if a.mode == "count":
             st = og.count()
@@ -35,7 +36,10 @@ def main():
             o = capi.run_options()
             capi._check(capi.lib().tl_aot_list(og._h, capi.C.byref(o), None, 0, 0, capi.C.byref(s)))
             st = s.as_dict()
-    print({k: st[k] for k in ("triangles", "probes", "probes_executed", "tasks", "list_ms", "prep_ms")})
+        best = st["list_ms"] if best is None else min(best, st["list_ms"])
+    d = {k: st[k] for k in ("triangles", "probes", "probes_executed", "tasks", "list_ms", "prep_ms")}
+    d["best_list_ms"] = best
+    print(d)
 
 
 if __name__ == "__main__":
