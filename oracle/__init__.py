@@ -150,19 +150,22 @@ def gen_config(cfg: dict) -> np.ndarray:
     raise ValueError(kind)
 
 
-def pairs_checksum(pairs: np.ndarray) -> dict:
+def pairs_checksum(pairs: np.ndarray, chunk: int = 1 << 24) -> dict:
     """Order-sensitive checksum of a pair list: sum and xor of
-    fmix64(i * 2^32 ... ) style keys, computed in numpy."""
-    p = pairs.astype(np.uint64)
-    idx = np.arange(p.shape[0], dtype=np.uint64)
-    with np.errstate(over="ignore"):
-        k = (p[:, 0] << np.uint64(32)) | p[:, 1]
-        k = k ^ (idx * np.uint64(0x9E3779B97F4A7C15))
-        k = (k ^ (k >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        k = (k ^ (k >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        k = k ^ (k >> np.uint64(31))
-        s = int(np.sum(k, dtype=np.uint64))
-    return {"sum": s, "xor": int(np.bitwise_xor.reduce(k))}
+    fmix64((u << 32 | v) ^ i * golden) over the pair index i (chunked)."""
+    s, x = 0, 0
+    for start in range(0, pairs.shape[0], chunk):
+        p = pairs[start:start + chunk].astype(np.uint64)
+        idx = np.arange(start, start + p.shape[0], dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            k = (p[:, 0] << np.uint64(32)) | p[:, 1]
+            k = k ^ (idx * np.uint64(0x9E3779B97F4A7C15))
+            k = (k ^ (k >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            k = (k ^ (k >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            k = k ^ (k >> np.uint64(31))
+            s = (s + int(np.sum(k, dtype=np.uint64))) & ((1 << 64) - 1)
+        x ^= int(np.bitwise_xor.reduce(k))
+    return {"sum": s, "xor": x}
 
 
 # --------------------------------------------------------------------------

@@ -42,13 +42,16 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #define TL_UNROLL 4  // rounds of 32 traversal loads in flight per warp
 #endif
 #ifndef TL_WARP_WORDS
-#define TL_WARP_WORDS 1536  // per-warp probe region in 32-bit words (6 KB)
+#define TL_WARP_WORDS 1280  // per-warp probe region in 32-bit words (5 KB: a 40,960-bit span)
 #endif
 #ifndef TL_CTAS_PER_SM
-#define TL_CTAS_PER_SM 4
+#define TL_CTAS_PER_SM 5
 #endif
 constexpr int kUnroll = TL_UNROLL;
-constexpr int kWarpThreads = 256;  // 8 warps per CTA
+#ifndef TL_WARP_CTA_THREADS
+#define TL_WARP_CTA_THREADS 256
+#endif
+constexpr int kWarpThreads = TL_WARP_CTA_THREADS;  // warps per CTA = kWarpThreads / 32
 constexpr int kWarpsPerCta = kWarpThreads / 32;
 constexpr uint32_t kWarpWords = TL_WARP_WORDS;
 constexpr uint32_t kWarpWordsLg = 31 - __builtin_clz(TL_WARP_WORDS);  // largest hash table: 2^lg <= words

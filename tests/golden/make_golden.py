@@ -35,15 +35,18 @@ def golden_for(key: str, threads: int) -> dict:
     t0 = time.time()
     pairs = O.gen_config(cfg)
     t_gen = time.time() - t0
+    checksum, first = pairs_checksum(pairs), pairs[:8].tolist()
+    npairs = int(pairs.shape[0])
     ref = O.RefGraph(cfg["n"], pairs)
+    del pairs  # host memory: the reference holds its own copies
     h = ref.hash(threads=threads)
     cm = ref.cost_model()
     out = {
         "config": key,
         "cfg": cfg,
-        "npairs": int(pairs.shape[0]),
-        "pairs_checksum": pairs_checksum(pairs),
-        "first_pairs": pairs[:8].tolist(),
+        "npairs": npairs,
+        "pairs_checksum": checksum,
+        "first_pairs": first,
         "n": ref.n,
         "m": ref.m,
         "max_out_degree": ref.max_out_degree(),
