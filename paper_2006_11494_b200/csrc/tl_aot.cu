@@ -65,7 +65,7 @@ constexpr uint32_t kCtaWords = 1u << kCtaWordsLg;  // 128 KB per CTA
 constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
 constexpr uint32_t kCtaHashDegMax = kCtaWords / 2;
 constexpr uint32_t kCtaStride = kCtaWords + 32;
-constexpr int kEmitCap = 64;     // per-warp staging of listed triangles
+constexpr int kEmitCap = 128;    // per-warp staging of hits (hash / list modes)
 constexpr uint32_t kShort = 32;  // claims of at most this length are packed
 constexpr uint64_t kTaskWarp = 4096;
 constexpr uint64_t kTaskCta = 65536;
@@ -190,7 +190,7 @@ template <AotMode MODE>
 struct Lane {
   uint32_t pos = 0, neg = 0;  // per record
   unsigned long long pos64 = 0, neg64 = 0, hsum = 0, hxor = 0;
-  uint32_t ebase = 0;   // LIST: byte address of the per-warp staging buffer
+  uint32_t ebase = 0;   // hash/list: byte address of the per-warp staging buffer
   uint32_t ecount = 0;  // warp-uniform
   __device__ __forceinline__ void fold() {
     pos64 += pos;
@@ -199,17 +199,38 @@ struct Lane {
   }
 };
 
+// Hash / list modes stage hits per warp as (pivot id, neighbour id, witness
+// rank); a flush maps the witnesses to original ids with independent gathers
+// (all in flight at once) and then hashes or writes the whole batch.
 template <AotMode MODE>
 __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
-  if constexpr (MODE == AotMode::list) {
+  if constexpr (MODE != AotMode::count) {
     __syncwarp();
     const uint32_t cnt = st.ecount;
     if (cnt) {
       unsigned long long base = 0;
-      if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
-      base = __shfl_sync(kFull, base, 0);
-      for (uint32_t i = lane_id(); i < 3 * cnt; i += 32) {
-        if (base + i / 3 < P.out_cap) P.out[3 * base + i] = ld_sm(st.ebase + 4 * i);
+      if constexpr (MODE == AotMode::list) {
+        if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
+        base = __shfl_sync(kFull, base, 0);
+      }
+#pragma unroll 4
+      for (uint32_t i = lane_id(); i < cnt; i += 32) {
+        const uint32_t e = st.ebase + 12 * i;
+        uint32_t a = ld_sm(e), b = ld_sm(e + 4);
+        uint32_t c = __ldg(P.orig + ld_sm(e + 8));
+        if constexpr (MODE == AotMode::list) {
+          if (base + i < P.out_cap) {
+            uint32_t* o = P.out + 3 * (base + i);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+          }
+        } else {
+          canon3(a, b, c);
+          const uint64_t h = tri_hash(a, b, c);
+          st.hsum += h;
+          st.hxor ^= h;
+        }
       }
     }
     st.ecount = 0;
@@ -223,27 +244,17 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
 template <AotMode MODE>
 __device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, uint32_t a_orig, uint32_t b_orig,
                                      uint32_t w) {
-  if constexpr (MODE == AotMode::hash) {
+  const unsigned hm = __ballot_sync(kFull, hit);
+  if (hm) {
+    const uint32_t k = __popc(hm);
+    if (st.ecount + k > kEmitCap) flush_emits(st, P);
     if (hit) {
-      uint32_t x = a_orig, y = b_orig, z = __ldg(P.orig + w);
-      canon3(x, y, z);
-      const uint64_t h = tri_hash(x, y, z);
-      st.hsum += h;
-      st.hxor ^= h;
+      const uint32_t slot = st.ebase + 12 * (st.ecount + __popc(hm & lanemask_lt()));
+      st_sm(slot, a_orig);
+      st_sm(slot + 4, b_orig);
+      st_sm(slot + 8, w);
     }
-  } else if constexpr (MODE == AotMode::list) {
-    const unsigned hm = __ballot_sync(kFull, hit);
-    if (hm) {
-      const uint32_t k = __popc(hm);
-      if (st.ecount + k > kEmitCap) flush_emits(st, P);
-      if (hit) {
-        const uint32_t slot = st.ebase + 12 * (st.ecount + __popc(hm & lanemask_lt()));
-        st_sm(slot, a_orig);
-        st_sm(slot + 4, b_orig);
-        st_sm(slot + 8, __ldg(P.orig + w));
-      }
-      st.ecount += k;
-    }
+    st.ecount += k;
   }
 }
 
@@ -393,7 +404,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
 }
 
 template <AotMode MODE>
-__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::list ? 3 : TL_CTAS_PER_SM) k_aot_warp(Params P) {
+__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS_PER_SM : 3) k_aot_warp(Params P) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
@@ -655,8 +666,8 @@ template <AotMode MODE>
 uint64_t launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
   uint64_t launches = 0;
   const size_t warp_smem =
-      sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE == AotMode::list ? kWarpsPerCta * 3 * kEmitCap : 0));
-  const size_t cta_smem = sizeof(uint32_t) * (kCtaStride + (MODE == AotMode::list ? kCtaWarps * 3 * kEmitCap : 0));
+      sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * kEmitCap : 0));
+  const size_t cta_smem = sizeof(uint32_t) * (kCtaStride + (MODE != AotMode::count ? kCtaWarps * 3 * kEmitCap : 0));
   TL_CUDA(cudaFuncSetAttribute(k_aot_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(warp_smem)));
   TL_CUDA(cudaFuncSetAttribute(k_aot_cta<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem)));
   const int sms = sm_count();
