@@ -28,6 +28,9 @@
 //     same cost prefix cuts the multi-GPU parts.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "tl_internal.cuh"
 
 namespace tlb {
@@ -58,17 +61,17 @@ constexpr uint32_t kWarpWordsLg = 31 - __builtin_clz(TL_WARP_WORDS);  // largest
 constexpr uint32_t kWarpSpanMax = kWarpWords * 32;                    // bitmap span
 constexpr uint32_t kWarpHashDegMax = (1u << kWarpWordsLg) / 2;
 constexpr uint32_t kWarpStride = kWarpWords + 32;    // + an always-zero guard word (128 B aligned)
-constexpr int kCtaThreads = 512;
-constexpr int kCtaWarps = kCtaThreads / 32;
-constexpr uint32_t kCtaWordsLg = 15;
-constexpr uint32_t kCtaWords = 1u << kCtaWordsLg;  // 128 KB per CTA
+// Phase 1 of the kernel: a CTA works on one heavy record with the union of
+// its warps' regions (the last guard stays past the end).
+constexpr uint32_t kCtaWords = kWarpsPerCta * kWarpStride - 32;
 constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
-constexpr uint32_t kCtaHashDegMax = kCtaWords / 2;
-constexpr uint32_t kCtaStride = kCtaWords + 32;
+constexpr uint32_t kCtaWordsLg = 31 - __builtin_clz(kCtaWords);
+constexpr uint32_t kCtaHashDegMax = (1u << kCtaWordsLg) / 2;
+constexpr uint64_t kCtaMinWork = 16384;  // wide-span pivots below this stay on the warp hash path
 constexpr int kEmitCap = 128;    // per-warp staging of hits (hash / list modes)
 constexpr uint32_t kShort = 32;  // claims of at most this length are packed
-constexpr uint64_t kTaskWarp = 4096;
-constexpr uint64_t kTaskCta = 65536;
+constexpr uint64_t kTaskMin = 4096;    // minimum work per warp task (adaptive: ~64 tasks per warp)
+constexpr uint64_t kCtaTaskScale = 8;  // a CTA record holds kCtaTaskScale warp tasks of work
 constexpr uint64_t kBeta = 2;    // staging weight per N+(l) element
 constexpr uint64_t kGamma = 64;  // per-record overhead
 constexpr uint64_t kKappa = 8;   // per-claim overhead (scheduling and the multi-GPU cut)
@@ -87,9 +90,11 @@ struct Params {
   const uint32_t* col;
   const uint2* claims;
   const uint32_t* orig;
-  const Rec* recs;
-  const uint2* tasks;  // warp kernel: [rb, re) record ranges
+  const Rec* recs;      // phase 2 (warp) records
+  const uint2* tasks;   // phase 2: [rb, re) record ranges
   uint64_t ntasks;
+  const Rec* crecs;     // phase 1 (CTA) records, one per task
+  uint64_t ncta;
   uint32_t skip_neg;
   unsigned long long* acc;
   uint32_t* out;
@@ -403,14 +408,73 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
   st.fold();
 }
 
+// ------------------------------------------------------------ the kernel
+// Persistent, two phases.  Phase 1: each CTA takes heavy records (wide spans
+// on big pivots) one at a time and probes them with all its warps against one
+// probe side built in the union of the warps' regions.  Phase 2: every warp
+// independently takes cost-balanced tasks of records with its own region.
+template <AotMode MODE, typename Probe>
+__device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
+                                           uint32_t a_orig, Lane<MODE>& st) {
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint64_t base = R.cb + 32 * warp; base < R.ce; base += 32 * kWarpsPerCta)
+    claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+}
+
 template <AotMode MODE>
-__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS_PER_SM : 3) k_aot_warp(Params P) {
+__device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32_t cbase, Lane<MODE>& st) {
+  const uint32_t* nl = P.col + R.lb;
+  const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
+  const uint32_t span = lmax - lmin + 1;
+  uint32_t a_orig = 0;
+  if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+  if (span <= kCtaSpanMax) {
+    for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) bitmap_set(cbase, lmin, __ldg(nl + i));
+    __syncthreads();
+    cta_claims(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
+    __syncthreads();
+    const uint32_t nwords = (span + 31) >> 5;
+    if (nwords <= max(uint32_t(kWarpThreads), 2 * R.dl))
+      for (uint32_t i = threadIdx.x; i < nwords; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
+    else
+      for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) bitmap_clear(cbase, lmin, __ldg(nl + i));
+  } else if (R.dl <= kCtaHashDegMax) {
+    uint32_t lg = 32 - __clz(2 * R.dl - 1);
+    lg = max(5u, min(lg, kCtaWordsLg));
+    const uint32_t cap = 1u << lg;
+    for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
+    __syncthreads();
+    cta_claims(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cap; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
+  } else {
+    cta_claims(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
+  }
+  st.fold();
+}
+
+template <AotMode MODE>
+__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS_PER_SM : 3) k_aot(Params P) {
+  __shared__ unsigned long long s_task;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
-  __syncwarp();
   Lane<MODE> st;
   st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (3 * kEmitCap));
+  __syncthreads();
+  // ---- phase 1: CTA records
+  if (P.ncta) {
+    const uint32_t cbase = sm_addr(0);
+    while (true) {
+      if (threadIdx.x == 0) s_task = atomicAdd(P.acc + kCtaCounter, 1ull);
+      __syncthreads();  // also orders the previous record's clear before the next build
+      const unsigned long long t = s_task;
+      __syncthreads();
+      if (t >= P.ncta) break;
+      cta_record(P, P.crecs[t], cbase, st);
+    }
+  }
+  // ---- phase 2: warp tasks
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(P.acc + kWarpCounter, 1ull);
@@ -418,66 +482,6 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS
     if (t >= P.ntasks) break;
     const uint2 tk = P.tasks[P.ntasks - 1 - t];  // heaviest pivots (highest ranks) first
     for (uint32_t r = tk.x; r < tk.y; ++r) warp_record(P, P.recs[r], wbase, st);
-  }
-  reduce_and_flush(st, P);
-}
-
-// ------------------------------------------------------------ CTA kernel
-// Heavy pivots (deg+ > 1024 and a span beyond the warp bitmap): one shared
-// probe side per CTA; the CTA's warps split the record's claims.
-template <AotMode MODE, typename Probe>
-__device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
-                                           uint32_t a_orig, Lane<MODE>& st) {
-  const uint32_t warp = threadIdx.x >> 5;
-  for (uint64_t base = R.cb + 32 * warp; base < R.ce; base += 32 * kCtaWarps)
-    claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
-}
-
-template <AotMode MODE>
-__global__ void __launch_bounds__(kCtaThreads, 1) k_aot_cta(Params P) {
-  __shared__ unsigned long long s_task;
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t cbase = sm_addr(0);
-  for (uint32_t i = threadIdx.x; i < kCtaStride; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
-  __syncthreads();
-  Lane<MODE> st;
-  st.ebase = sm_addr(kCtaStride + warp * (3 * kEmitCap));
-  while (true) {
-    if (threadIdx.x == 0) s_task = atomicAdd(P.acc + kCtaCounter, 1ull);
-    __syncthreads();
-    const unsigned long long t = s_task;
-    __syncthreads();
-    if (t >= P.ntasks) break;
-    const Rec R = P.recs[t];
-    const uint32_t* nl = P.col + R.lb;
-    const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
-    const uint32_t span = lmax - lmin + 1;
-    uint32_t a_orig = 0;
-    if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
-    if (span <= kCtaSpanMax) {
-      for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) bitmap_set(cbase, lmin, __ldg(nl + i));
-      __syncthreads();
-      cta_claims(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
-      __syncthreads();
-      const uint32_t nwords = (span + 31) >> 5;
-      if (nwords <= max(uint32_t(kCtaThreads), 2 * R.dl))
-        for (uint32_t i = threadIdx.x; i < nwords; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
-      else
-        for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) bitmap_clear(cbase, lmin, __ldg(nl + i));
-    } else if (R.dl <= kCtaHashDegMax) {
-      uint32_t lg = 32 - __clz(2 * R.dl - 1);
-      lg = max(5u, min(lg, kCtaWordsLg));
-      const uint32_t cap = 1u << lg;
-      for (uint32_t i = threadIdx.x; i < R.dl; i += kCtaThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
-      __syncthreads();
-      cta_claims(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
-      __syncthreads();
-      for (uint32_t i = threadIdx.x; i < cap; i += kCtaThreads) st_sm(cbase + 4 * i, 0u);
-    } else {
-      cta_claims(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
-    }
-    st.fold();
-    __syncthreads();
   }
   reduce_and_flush(st, P);
 }
@@ -574,13 +578,16 @@ __global__ void k_logical(const uint2* claims, const uint64_t* off, uint64_t cb,
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
 }
 
-__device__ __forceinline__ bool warp_path(uint32_t dl, uint32_t span) {
-  return span <= kWarpSpanMax || dl <= kWarpHashDegMax;
+// Warp path: the span fits the warp bitmap, or a small pivot (warp hash) with
+// too little work to occupy a CTA.  Everything else is a phase-1 CTA record.
+__device__ __forceinline__ bool warp_path(uint32_t dl, uint32_t span, uint64_t work) {
+  return span <= kWarpSpanMax || (dl <= kWarpHashDegMax && work < kCtaMinWork);
 }
 
 // Per pivot of the part: number of warp records / CTA records.
 __global__ void k_classify(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, const uint32_t* col,
-                           uint32_t pb, uint32_t np, uint64_t cb, uint64_t ce, uint32_t* nrw, uint32_t* nrc) {
+                           uint32_t pb, uint32_t np, uint64_t cb, uint64_t ce, uint64_t T, uint32_t* nrw,
+                           uint32_t* nrc) {
   TL_GRID_STRIDE(i, uint64_t(np) + 1) {
     uint32_t nw = 0, nc = 0;
     if (i < np) {
@@ -592,14 +599,38 @@ __global__ void k_classify(const uint64_t* CP, const uint64_t* claim_off, const 
       const uint32_t dl = uint32_t(off[l + 1] - lb);
       if (W && dl) {
         const uint32_t span = col[lb + dl - 1] - col[lb] + 1;
-        if (warp_path(dl, span))
-          nw = uint32_t((Wk + kTaskWarp - 1) / kTaskWarp);
+        if (warp_path(dl, span, Wk))
+          nw = uint32_t((Wk + T - 1) / T);
         else
-          nc = uint32_t((Wk + kTaskCta - 1) / kTaskCta);
+          nc = uint32_t((Wk + kCtaTaskScale * T - 1) / (kCtaTaskScale * T));
       }
     }
     nrw[i] = nw;
     nrc[i] = nc;
+  }
+}
+
+// Diagnostic (TL_DEBUG_PATHS=1): windowed work W per probe path and per
+// log2(span) bucket.  out[0..4] = warp bitmap, warp hash, CTA bitmap, CTA
+// hash, global search; out[8 + b] = work with ceil(log2(span)) == b.
+__global__ void k_path_stats(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, const uint32_t* col,
+                             uint32_t pb, uint32_t np, uint64_t cb, uint64_t ce, unsigned long long* out) {
+  TL_GRID_STRIDE(i, uint64_t(np)) {
+    const uint32_t l = pb + uint32_t(i);
+    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
+    const uint64_t W = a < b ? CP[b] - CP[a] : 0;
+    const uint64_t lb = off[l];
+    const uint32_t dl = uint32_t(off[l + 1] - lb);
+    if (!W || !dl) continue;
+    const uint32_t span = col[lb + dl - 1] - col[lb] + 1;
+    int path;
+    if (span <= kWarpSpanMax) path = 0;
+    else if (warp_path(dl, span, W + kKappa * (b - a))) path = 1;
+    else if (span <= kCtaSpanMax) path = 2;
+    else if (dl <= kCtaHashDegMax) path = 3;
+    else path = 4;
+    atomicAdd(out + path, (unsigned long long)W);
+    atomicAdd(out + 8 + (32 - __clz(span - 1 | 1)), (unsigned long long)W);
   }
 }
 
@@ -638,10 +669,10 @@ __global__ void k_records(const uint64_t* CP, const uint64_t* claim_off, const u
 }
 
 // Task g = the warp records whose weight prefix RP lies in [g*T, (g+1)*T).
-__global__ void k_tasks(const uint64_t* RP, uint32_t nrec, uint64_t G, uint2* tasks) {
+__global__ void k_tasks(const uint64_t* RP, uint32_t nrec, uint64_t G, uint64_t T, uint2* tasks) {
   TL_GRID_STRIDE(g, G) {
-    const uint64_t lo = lower_bound_u64(RP, 0, nrec, g * kTaskWarp);
-    const uint64_t hi = g + 1 == G ? nrec : lower_bound_u64(RP, 0, nrec, (g + 1) * kTaskWarp);
+    const uint64_t lo = lower_bound_u64(RP, 0, nrec, g * T);
+    const uint64_t hi = g + 1 == G ? nrec : lower_bound_u64(RP, 0, nrec, (g + 1) * T);
     tasks[g] = make_uint2(uint32_t(lo), uint32_t(hi));
   }
 }
@@ -663,31 +694,27 @@ int sm_count() {
 }
 
 template <AotMode MODE>
-uint64_t launch_kernels(const Params& pw, const Params& pc, cudaStream_t s) {
-  uint64_t launches = 0;
-  const size_t warp_smem =
-      sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * kEmitCap : 0));
-  const size_t cta_smem = sizeof(uint32_t) * (kCtaStride + (MODE != AotMode::count ? kCtaWarps * 3 * kEmitCap : 0));
-  TL_CUDA(cudaFuncSetAttribute(k_aot_warp<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(warp_smem)));
-  TL_CUDA(cudaFuncSetAttribute(k_aot_cta<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cta_smem)));
-  const int sms = sm_count();
-  if (pc.ntasks) {
-    const unsigned grid = unsigned(std::min<uint64_t>(pc.ntasks, uint64_t(sms)));
-    k_aot_cta<MODE><<<grid, kCtaThreads, cta_smem, s>>>(pc);
-    TL_CUDA(cudaGetLastError());
-    ++launches;
-  }
-  if (pw.ntasks) {
-    int per_sm = 0;
-    TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot_warp<MODE>, kWarpThreads, warp_smem));
-    per_sm = std::max(per_sm, 1);
-    const uint64_t want = (pw.ntasks + kWarpsPerCta - 1) / kWarpsPerCta;
-    const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sms) * per_sm));
-    k_aot_warp<MODE><<<grid, kWarpThreads, warp_smem, s>>>(pw);
-    TL_CUDA(cudaGetLastError());
-    ++launches;
-  }
-  return launches;
+size_t kernel_smem() {
+  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * kEmitCap : 0));
+}
+
+template <AotMode MODE>
+int resident_warps() {  // warps of k_aot<MODE> the device keeps resident
+  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kernel_smem<MODE>())));
+  int per_sm = 0;
+  TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot<MODE>, kWarpThreads, kernel_smem<MODE>()));
+  return sm_count() * std::max(per_sm, 1) * kWarpsPerCta;
+}
+
+template <AotMode MODE>
+uint64_t launch_kernels(const Params& P, cudaStream_t s) {
+  if (!P.ntasks && !P.ncta) return 0;
+  const uint64_t ctas = uint64_t(resident_warps<MODE>()) / kWarpsPerCta;
+  const uint64_t want = std::max<uint64_t>(P.ncta, (P.ntasks + kWarpsPerCta - 1) / kWarpsPerCta);
+  const unsigned grid = unsigned(std::min<uint64_t>(want, ctas));
+  k_aot<MODE><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
+  TL_CUDA(cudaGetLastError());
+  return 1;
 }
 
 }  // namespace
@@ -749,6 +776,23 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     }
   }
 
+  // adaptive task size: ~64 warp tasks per resident warp
+  uint64_t T = kTaskMin;
+  {
+    uint64_t w[2] = {0, 0};
+    TL_CUDA(cudaMemcpyAsync(w, CP.p + cb, 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaMemcpyAsync(w + 1, CP.p + ce, 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+    const uint64_t work = (w[1] - w[0]) + kKappa * (ce - cb);
+    int warps = 0;
+    switch (mode) {
+      case AotMode::count: warps = resident_warps<AotMode::count>(); break;
+      case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
+      case AotMode::list: warps = resident_warps<AotMode::list>(); break;
+    }
+    T = std::max<uint64_t>(kTaskMin, work / (uint64_t(std::max(warps, 1)) * 64));
+  }
+
   const uint32_t np = cb < ce ? pe - pb : 0;
   DBuf<uint32_t> nrw, nrc, ow, oc;
   DBuf<Rec> wrecs, crecs;
@@ -761,10 +805,26 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     ow.alloc(np + 1, s);
     oc.alloc(np + 1, s);
     k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, og.col.p,
-                                                                          pb, np, cb, ce, nrw.p, nrc.p);
+                                                                          pb, np, cb, ce, T, nrw.p, nrc.p);
     TL_CUDA(cudaGetLastError());
     cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrw.p, ow.p, np + 1, s); });
     cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrc.p, oc.p, np + 1, s); });
+    if (getenv("TL_DEBUG_PATHS")) {
+      DBuf<unsigned long long> ps;
+      ps.alloc(48, s);
+      TL_CUDA(cudaMemsetAsync(ps.p, 0, 48 * 8, s));
+      k_path_stats<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, og.col.p, pb, np, cb,
+                                                                ce, ps.p);
+      unsigned long long hp[48];
+      TL_CUDA(cudaMemcpyAsync(hp, ps.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "[tl paths] warp-bitmap %llu warp-hash %llu cta-bitmap %llu cta-hash %llu global %llu\n", hp[0],
+              hp[1], hp[2], hp[3], hp[4]);
+      fprintf(stderr, "[tl span log2 buckets]");
+      for (int b = 0; b < 40; ++b)
+        if (hp[8 + b]) fprintf(stderr, " %d:%llu", b, hp[8 + b]);
+      fprintf(stderr, "\n");
+    }
     uint32_t tw = 0, tc = 0;
     TL_CUDA(cudaMemcpyAsync(&tw, ow.p + np, 4, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaMemcpyAsync(&tc, oc.p + np, 4, cudaMemcpyDeviceToHost, s));
@@ -783,9 +843,9 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
       uint64_t total = 0;
       TL_CUDA(cudaMemcpyAsync(&total, wgt.p + nw, 8, cudaMemcpyDeviceToHost, s));
       TL_CUDA(cudaStreamSynchronize(s));
-      G = total ? (total - 1) / kTaskWarp + 1 : 0;
+      G = total ? (total - 1) / T + 1 : 0;
       tasks.alloc(std::max<uint64_t>(G, 1), s);
-      if (G) k_tasks<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(wgt.p, uint32_t(nw), G, tasks.p);
+      if (G) k_tasks<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(wgt.p, uint32_t(nw), G, T, tasks.p);
       TL_CUDA(cudaGetLastError());
       r.launches += 1 + 2 + (G ? 1 : 0);
     }
@@ -808,16 +868,15 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   P.acc = acc.p;
   P.out = d_out;
   P.out_cap = out_cap;
-  Params pw = P, pc = P;
-  pw.recs = wrecs.p;
-  pw.tasks = tasks.p;
-  pw.ntasks = G;
-  pc.recs = crecs.p;
-  pc.ntasks = nc;
+  P.recs = wrecs.p;
+  P.tasks = tasks.p;
+  P.ntasks = G;
+  P.crecs = crecs.p;
+  P.ncta = nc;
   switch (mode) {
-    case AotMode::count: r.launches += launch_kernels<AotMode::count>(pw, pc, s); break;
-    case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(pw, pc, s); break;
-    case AotMode::list: r.launches += launch_kernels<AotMode::list>(pw, pc, s); break;
+    case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, s); break;
+    case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, s); break;
+    case AotMode::list: r.launches += launch_kernels<AotMode::list>(P, s); break;
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];
