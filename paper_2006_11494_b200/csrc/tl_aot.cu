@@ -50,6 +50,9 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #ifndef TL_CTAS_PER_SM
 #define TL_CTAS_PER_SM 5
 #endif
+#ifndef TL_CTA_MIN_WORK
+#define TL_CTA_MIN_WORK 65536
+#endif
 constexpr int kUnroll = TL_UNROLL;
 #ifndef TL_WARP_CTA_THREADS
 #define TL_WARP_CTA_THREADS 256
@@ -67,7 +70,7 @@ constexpr uint32_t kCtaWords = kWarpsPerCta * kWarpStride - 32;
 constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
 constexpr uint32_t kCtaWordsLg = 31 - __builtin_clz(kCtaWords);
 constexpr uint32_t kCtaHashDegMax = (1u << kCtaWordsLg) / 2;
-constexpr uint64_t kCtaMinWork = 16384;  // wide-span pivots below this stay on the warp hash path
+constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below this stay on the warp hash path
 constexpr int kEmitCap = 128;    // per-warp staging of hits (hash / list modes)
 constexpr uint32_t kShort = 32;  // claims of at most this length are packed
 constexpr uint64_t kTaskMin = 4096;    // minimum work per warp task (adaptive: ~64 tasks per warp)
@@ -88,7 +91,8 @@ enum Acc : int { kPos = 0, kNeg, kExec, kHsum, kHxor, kEmitted, kWarpCounter, kC
 struct Params {
   const uint64_t* off;
   const uint32_t* col;
-  const uint2* claims;
+  const uint64_t* win;     // claim windows {begin:40 | len:23 | neg:1}
+  const uint32_t* cs;      // traversed vertex per claim (hash/list modes)
   const uint32_t* orig;
   const Rec* recs;      // phase 2 (warp) records
   const uint2* tasks;   // phase 2: [rb, re) record ranges
@@ -271,23 +275,19 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
                                             uint64_t base, uint64_t ce, Lane<MODE>& st) {
   const uint32_t lane = lane_id();
   const uint64_t c = base + lane;
-  uint32_t sflag = 0;
   uint64_t b = 0;
   uint32_t len = 0;
+  bool neg = false;
   if (c < ce) {
-    const uint2 cl = P.claims[c];
-    sflag = cl.x;
-    if (!(P.skip_neg && (sflag & kNegBit))) {
-      const uint32_t s = sflag & ~kNegBit;
-      const uint64_t os = P.off[s], e = P.off[s + 1];
-      b = os + cl.y;
-      len = e > b ? uint32_t(e - b) : 0;
-    }
+    const uint64_t w = P.win[c];
+    b = w & kWinBeginMask;
+    neg = w >> 63;
+    len = (P.skip_neg && neg) ? 0u : uint32_t((w >> kWinLenShift) & kWinLenMask);
   }
-  const bool neg = sflag & kNegBit;
+  const uint32_t sflag = neg ? kNegBit : 0u;
   uint32_t b_orig = 0;
   if constexpr (MODE != AotMode::count) {
-    if (len) b_orig = __ldg(P.orig + (sflag & ~kNegBit));
+    if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit));
   }
 
   // ---- short claims: 32 probes per round, load-balanced over the lanes
@@ -492,18 +492,19 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS
 
 // Claim cost (window upper bound): deg+(s) - pos; 0 for skipped negative
 // claims.  With `logical`, also sums the logical probes (deg+(s) per claim).
-__global__ void k_claim_cost(const uint2* claims, const uint64_t* off, uint64_t m, uint32_t skip_neg, uint64_t* cost,
-                             unsigned long long* logical) {
+__global__ void k_claim_cost(const uint64_t* win, const uint32_t* cs, const uint64_t* off, uint64_t m,
+                             uint32_t skip_neg, uint64_t* cost, unsigned long long* logical) {
   unsigned long long lsum = 0;
   TL_GRID_STRIDE(i, m + 1) {
     uint64_t c = 0;
     if (i < m) {
-      const uint2 cl = claims[i];
-      if (!(skip_neg && (cl.x & kNegBit))) {
-        const uint32_t s = cl.x & ~kNegBit;
-        const uint64_t d = off[s + 1] - off[s];
-        c = d - cl.y;
-        lsum += d;
+      const uint64_t w = win[i];
+      if (!(skip_neg && (w >> 63))) {
+        c = (w >> kWinLenShift) & kWinLenMask;
+        if (logical) {
+          const uint32_t s = cs[i] & ~kNegBit;
+          lsum += off[s + 1] - off[s];
+        }
       }
     }
     cost[i] = c;
@@ -564,13 +565,13 @@ __global__ void k_split(const uint64_t* CP, uint64_t m, const uint64_t* claim_of
 
 // Logical probes (engine.hpp:250/:264: one per element of the full traversed
 // list) over the part's claims.
-__global__ void k_logical(const uint2* claims, const uint64_t* off, uint64_t cb, uint64_t ce, uint32_t skip_neg,
+__global__ void k_logical(const uint32_t* cs, const uint64_t* off, uint64_t cb, uint64_t ce, uint32_t skip_neg,
                           unsigned long long* acc) {
   unsigned long long sum = 0;
   TL_GRID_STRIDE(k, ce - cb) {
-    const uint2 cl = claims[cb + k];
-    if (!(skip_neg && (cl.x & kNegBit))) {
-      const uint32_t s = cl.x & ~kNegBit;
+    const uint32_t sflag = cs[cb + k];
+    if (!(skip_neg && (sflag & kNegBit))) {
+      const uint32_t s = sflag & ~kNegBit;
       sum += off[s + 1] - off[s];
     }
   }
@@ -699,11 +700,17 @@ size_t kernel_smem() {
 }
 
 template <AotMode MODE>
-int resident_warps() {  // warps of k_aot<MODE> the device keeps resident
+int resident_warps() {  // warps of k_aot<MODE> the current device keeps resident (cached per device)
+  static int cache[64] = {0};
+  int dev = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
   TL_CUDA(cudaFuncSetAttribute(k_aot<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kernel_smem<MODE>())));
   int per_sm = 0;
   TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot<MODE>, kWarpThreads, kernel_smem<MODE>()));
-  return sm_count() * std::max(per_sm, 1) * kWarpsPerCta;
+  const int w = sm_count() * std::max(per_sm, 1) * kWarpsPerCta;
+  if (dev >= 0 && dev < 64) cache[dev] = w;
+  return w;
 }
 
 template <AotMode MODE>
@@ -745,8 +752,8 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   DBuf<uint64_t> CP;
   CP.alloc(m + 1, s);
   const bool whole = nparts == 1;
-  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.claims.p, og.off.p, m, skip_negative, CP.p,
-                                                               whole ? acc.p + kLogical : nullptr);
+  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.win.p, og.claim_s.p, og.off.p, m, skip_negative,
+                                                               CP.p, whole ? acc.p + kLogical : nullptr);
   TL_CUDA(cudaGetLastError());
   cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, CP.p, m + 1, s); });
   r.launches += 1 + 2;  // k_claim_cost, scan (init + sweep)
@@ -769,7 +776,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     r.table_builds = hs[6];
     ++r.launches;
     if (cb < ce) {
-      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claims.p, og.off.p, cb, ce, skip_negative,
+      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claim_s.p, og.off.p, cb, ce, skip_negative,
                                                                  acc.p + kLogical);
       TL_CUDA(cudaGetLastError());
       ++r.launches;
@@ -862,7 +869,8 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   Params P{};
   P.off = og.off.p;
   P.col = og.col.p;
-  P.claims = og.claims.p;
+  P.win = og.win.p;
+  P.cs = og.claim_s.p;
   P.orig = og.orig.p;
   P.skip_neg = skip_negative;
   P.acc = acc.p;

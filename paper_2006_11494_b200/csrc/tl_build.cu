@@ -250,6 +250,20 @@ __global__ void k_claims(uint64_t* dk_val, uint32_t* ckey, uint64_t m, uint32_t 
   }
 }
 
+// Claim windows: after grouping, each claim (pos << 32 | s | neg << 31)
+// becomes the packed traversal window {begin:40 | len:23 | neg:1} (in place)
+// plus the traversed vertex id (s | neg << 31) for the hash/list modes.
+__global__ void k_windows(uint64_t* val_win, uint64_t m, const uint64_t* off, uint32_t* cs) {
+  TL_GRID_STRIDE(i, m) {
+    const uint64_t v = val_win[i];
+    const uint32_t sflag = uint32_t(v), pos = uint32_t(v >> 32);
+    const uint32_t s = sflag & ~kNegBit;
+    const uint64_t b = off[s] + pos, len = off[s + 1] - b;
+    cs[i] = sflag;
+    val_win[i] = b | (len << kWinLenShift) | (uint64_t(sflag >> 31) << 63);
+  }
+}
+
 // ------------------------------------------------ reference-layout transfer
 __global__ void k_rank_degrees(const uint32_t* orig, uint32_t n, const uint64_t* out_off, uint64_t* deg) {
   TL_GRID_STRIDE(r, uint64_t(n) + 1) {
@@ -589,7 +603,8 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   TL_CUDA(cudaMemsetAsync(scal.p, 0, 32, s));
   if (m == 0) {
     TL_CUDA(cudaMemsetAsync(og.claim_off.p, 0, sizeof(uint64_t) * (uint64_t(og.n) + 1), s));
-    og.claims.alloc(1, s);
+    og.win.alloc(1, s);
+    og.claim_s.alloc(1, s);
     og.max_out_degree = 0;
     og.cost[0] = og.cost[1] = og.cost[2] = 0;
     return;
@@ -612,18 +627,19 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   ckey2.reset();
   val2.reset();
   fill_offsets(ckey.p, 0, m, og.n, og.claim_off.p, s);
-  // claims take over the value buffer: (pos << 32 | s) == uint2{s, pos}
-  og.claims.reset();
-  og.claims.p = reinterpret_cast<uint2*>(dk.p);
-  og.claims.n = dk.n;
-  og.claims.s = dk.s;
-  dk.p = nullptr;
-  dk.n = 0;
   TL_CUDA(cudaStreamSynchronize(s));
   og.cost[0] = host[0];
   og.cost[1] = host[1];
   og.cost[2] = host[2];
   og.max_out_degree = uint32_t(host[3]);
+  TL_REQUIRE(m < (1ull << kWinLenShift) && og.max_out_degree < (1u << 23), TL_EINVAL,
+             "graph exceeds the claim-window encoding (m < 2^40, max out-degree < 2^23)");
+  // windows are written over the sorted values; the key buffer becomes claim_s
+  k_windows<<<grid_for(m, kBlock, 148u * 64u), kBlock, 0, s>>>(dk.p, m, og.off.p, ckey.p);
+  TL_CUDA(cudaGetLastError());
+  og.win = std::move(dk);
+  og.claim_s = std::move(ckey);
+  TL_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace

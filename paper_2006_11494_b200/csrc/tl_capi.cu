@@ -107,7 +107,8 @@ tl_oriented::~tl_oriented() {
   orig.reset();
   rank.reset();
   claim_off.reset();
-  claims.reset();
+  win.reset();
+  claim_s.reset();
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

@@ -42,7 +42,8 @@ struct tl_oriented {
   tlb::DBuf<uint32_t> orig;       // n: rank -> original id
   tlb::DBuf<uint32_t> rank;       // n: original id -> rank
   tlb::DBuf<uint64_t> claim_off;  // n+1, by pivot
-  tlb::DBuf<uint2> claims;        // m: x = s | neg << 31, y = start position in N+(s)
+  tlb::DBuf<uint64_t> win;        // m claim windows {begin:40 | len:23 | neg:1} into col
+  tlb::DBuf<uint32_t> claim_s;    // m traversed vertex ids s | neg << 31
   // triangle count per (skip_negative, part, nparts): sizes listing buffers
   std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
   ~tl_oriented();
@@ -51,6 +52,9 @@ struct tl_oriented {
 namespace tlb {
 
 constexpr uint32_t kNegBit = 0x80000000u;
+constexpr uint32_t kWinLenShift = 40;
+constexpr uint64_t kWinBeginMask = (1ull << kWinLenShift) - 1;
+constexpr uint64_t kWinLenMask = (1ull << 23) - 1;
 
 struct DeviceGuard {
   int prev = 0;
