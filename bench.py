@@ -3,8 +3,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
-Workload: BASELINE.json configs[1] (R-MAT scale 20, edge factor 16) by
-default, generated on the device from its seed (inputs resident in HBM).  A
+Workload: BASELINE.json configs[3] (R-MAT scale 26, edge factor 16) by default
+-- the config the metric ("... 1/2/4/8 B200") is quoted on, and it fits one
+GPU -- generated on the device from its seed (inputs resident in HBM).  A
 step is one AOT counting run over the oriented graph -- the C-ABI call that
 replaces run_parallel_count (task construction + intersection kernels + the
 stats read-back), on this rank's cost-balanced share of the directed edges.
@@ -45,7 +46,7 @@ def parse_args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--no-list", action="store_true", help="skip the listing-mode measurement")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -192,6 +193,76 @@ def run_reference_arm(args):
 
 
 # ----------------------------------------------------------------- GPU side
+def gpath_ok(config: str) -> bool:
+    path = os.path.join(ROOT, "tests", "golden", "configs.json")
+    return os.path.exists(path) and config in json.load(open(path))
+
+
+def run_e2e(args, og, n, m, rank, world, local, dev, sp, flush, barrier, max_ranks):
+    import numpy as np
+    import torch
+
+    from paper_2006_11494_b200 import capi
+
+    job = os.environ.get("TORCHELASTIC_RUN_ID", str(os.getppid()))
+    base = f"/dev/shm/trilist_e2e_{job}"
+    names = {"out_offsets": np.uint64, "out": np.uint32, "rank": np.uint32}
+    if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+        host = og.csr()  # device -> host once: the reference layout a caller would hold
+        for k in names:
+            host[k].tofile(f"{base}_{k}.bin")
+        del host
+    og.close()
+    torch.cuda.empty_cache()
+    barrier()
+    cudart = torch.cuda.cudart()
+    maps, ptrs, et, launches = {}, {}, [], 0
+    try:
+        for k, dt in names.items():
+            a = np.memmap(f"{base}_{k}.bin", dtype=dt, mode="r+")  # shared tmpfs pages, never written
+            maps[k] = a
+            rc = cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)  # page-lock for DMA
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister failed ({int(rc)})")
+            ptrs[k] = a.ctypes.data
+        h2d = sum(a.nbytes for a in maps.values())
+        d2h = capi.C.sizeof(capi.TlStats)
+
+        def step():
+            up = capi.DeviceOriented.from_host_ptrs(n, m, ptrs["out_offsets"], ptrs["out"], ptrs["rank"], local, sp)
+            st = up.count(part=rank, nparts=world, stream=sp)
+            up.close()
+            return st
+
+        for _ in range(max(1, args.warmup // 2)):
+            step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            st = step()
+            et.append(time.perf_counter() - t0)
+            launches += st["kernel_launches"]
+        barrier()
+    finally:
+        for p in ptrs.values():
+            cudart.cudaHostUnregister(p)
+        maps.clear()
+        if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+            for k in names:
+                try:
+                    os.unlink(f"{base}_{k}.bin")
+                except OSError:
+                    pass
+    e_s = max_ranks(statistics.mean(et))
+    return {"value": m / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": e_s * 1e3, "launches": launches,
+            "path": "tl_oriented_from_csr (pinned host reference layout, shared by the node's ranks) + "
+                    "tl_aot_count + stats read-back"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -232,12 +303,13 @@ def run_ours(args):
     t0 = time.perf_counter()
     dg = capi.DeviceGraph.from_device_pairs(d_pairs.data_ptr(), cfg["npairs"], cfg["n"], local, sp)
     phases["from_edges_ms"] = (time.perf_counter() - t0) * 1e3
+    del d_pairs  # the largest configs need the HBM for orient()
+    torch.cuda.empty_cache()
     t0 = time.perf_counter()
     og = dg.orient()
     phases["order_orient_claims_ms"] = (time.perf_counter() - t0) * 1e3
     n, m = og.n, og.m
     costs = og.cost_model()
-    del d_pairs
     dg.close()
     torch.cuda.empty_cache()
 
@@ -281,63 +353,57 @@ def run_ours(args):
     # parity of this run against the reference's golden values (when present)
     parity = None
     gpath = os.path.join(ROOT, "tests", "golden", "configs.json")
-    if os.path.exists(gpath):
+    if gpath_ok(args.config):
         g = json.load(open(gpath)).get(args.config)
         if g:
             parity = all(whole[k] == g[k] for k in ("triangles", "probes", "positive_triangles",
                                                     "negative_triangles", "table_builds"))
 
-    # ---- listing (emission to an HBM buffer, 12 B per triangle)
+    # ---- listing: triangles emitted into an HBM buffer (12 B each) when the
+    #      list fits in a quarter of the free HBM, otherwise emitted into the
+    #      order-independent hash (the large configs' "list with hash").
     list_info = None
     if not args.no_list:
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        materialise = 12 * T / world < free_b / 4
+        mode = "list" if materialise else "hash"
+
         def list_step():
             s = capi.TlStats()
             o = capi.run_options(False, rank, world, sp)
-            capi._check(capi.lib().tl_aot_list(og._h, capi.C.byref(o), None, 0, 0, capi.C.byref(s)))
+            if materialise:
+                capi._check(capi.lib().tl_aot_list(og._h, capi.C.byref(o), None, 0, 0, capi.C.byref(s)))
+            else:
+                capi._check(capi.lib().tl_aot_hash(og._h, capi.C.byref(o), capi.C.byref(s)))
             return s.as_dict()
 
         lt, ls = timed(list_step, max(3, args.steps // 2), max(1, args.warmup // 2))
         l_step = max_ranks(statistics.mean(lt))
         l_kern = max_ranks(statistics.mean(s["list_ms"] for s in ls))
         launches += sum(s["kernel_launches"] for s in ls)
-        list_info = {"ms_per_step": l_step, "kernel_ms": l_kern, "triangles_per_s": T / (l_step * 1e-3),
+        hashed = tdist.reduce_stats(ls[-1]) if world > 1 else ls[-1]
+        b_list = B["list"] if materialise else B["count"]
+        list_info = {"mode": mode, "ms_per_step": l_step, "kernel_ms": l_kern, "triangles_per_s": T / (l_step * 1e-3),
                      "directed_edges_per_s": m / (l_step * 1e-3),
-                     "roofline_frac": (B["list"] / world) / (l_kern * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+                     "roofline_frac": (b_list / world) / (l_kern * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+        if not materialise:
+            list_info["hash"] = {"count": hashed["triangles"], "sum": hashed["hash_sum"], "xor": hashed["hash_xor"]}
+            if gpath_ok(args.config):
+                g = json.load(open(gpath)).get(args.config)
+                list_info["hash_matches_reference"] = (hashed["hash_sum"], hashed["hash_xor"]) == (
+                    g["hash_sum"], g["hash_xor"])
 
-    # ---- e2e through the C-ABI with host (pinned) buffers
+    # ---- e2e through the C-ABI with host buffers: every step uploads the
+    #      reference-layout OrientedGraph from pinned host memory, counts, and
+    #      reads the stats back.  The host copy is shared by the ranks of the
+    #      node through /dev/shm (one copy, pinned by every rank); the
+    #      device-resident graph is released first (the upload rebuilds one).
     e2e = None
     if not args.no_e2e:
-        host = og.csr()
-        t_off = torch.from_numpy(host["out_offsets"].view(np.int64)).pin_memory()
-        t_out = torch.from_numpy(host["out"].view(np.int32)).pin_memory()
-        t_rank = torch.from_numpy(host["rank"].view(np.int32)).pin_memory()
-        h2d = t_off.numel() * 8 + t_out.numel() * 4 + t_rank.numel() * 4
-        d2h = capi.C.sizeof(capi.TlStats)
-
-        def e2e_step():
-            up = capi.DeviceOriented.from_host_ptrs(n, m, t_off.data_ptr(), t_out.data_ptr(), t_rank.data_ptr(),
-                                                    local, sp)
-            st = up.count(part=rank, nparts=world, stream=sp)
-            up.close()
-            return st
-
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        torch.cuda.synchronize(dev)
-        barrier()
-        et = []
-        for _ in range(max(3, args.steps // 2)):
-            flush.fill_(1)
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            st = e2e_step()
-            et.append(time.perf_counter() - t0)
-            launches += st["kernel_launches"]
-        barrier()
-        e_s = max_ranks(statistics.mean(et))
-        e2e = {"value": m / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e_s * 1e3,
-               "path": "tl_oriented_from_csr (pinned host reference layout) + tl_aot_count + stats read-back"}
+        e2e = run_e2e(args, og, n, m, rank, world, local, dev, sp, flush, barrier, max_ranks)
+        launches += e2e.pop("launches")
+    og.close()
+    torch.cuda.empty_cache()
 
     # ---- CPU baseline: the reference library on this host (rank 0, N=1)
     cpu = None

@@ -23,8 +23,18 @@ def main():
     d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
     capi.gen_pairs_device(cfg, d.data_ptr())
     torch.cuda.synchronize()
-    og = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"]).orient()
+    import time
+
+    t0 = time.time()
+    g = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"])
+    t1 = time.time()
     del d
+    torch.cuda.empty_cache()
+    og = g.orient()
+    t2 = time.time()
+    g.close()
+    print({"n": og.n, "m": og.m, "from_edges_s": round(t1 - t0, 3), "orient_s": round(t2 - t1, 3),
+           "max_out_degree": og.max_out_degree, "cost": og.cost_model()}, flush=True)
     best = None
     for _ in range(a.reps):
         if a.mode == "count":
