@@ -301,22 +301,33 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   const uint32_t excl = incl - slen;
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   const uint64_t bm = b - excl;  // element q of the packed stream: col[bm(owner) + q]
-  for (uint32_t r0 = 0; r0 < total; r0 += 32) {
-    const uint32_t q = r0 + lane;
-    uint32_t i = 0;  // owner: the largest lane i with excl_i <= q
+#ifndef TL_SHORT_UNROLL
+#define TL_SHORT_UNROLL 1
+#endif
+  constexpr int kSU = TL_SHORT_UNROLL;  // packed rounds in flight
+  for (uint32_t r0 = 0; r0 < total; r0 += 32 * kSU) {
+    uint32_t x[kSU], of[kSU], oo[kSU];
 #pragma unroll
-    for (uint32_t step = 16; step; step >>= 1) {
-      const uint32_t pv = __shfl_sync(kFull, excl, i + step);
-      if (pv <= q) i += step;
+    for (int k = 0; k < kSU; ++k) {
+      const uint32_t q = r0 + 32 * k + lane;
+      uint32_t i = 0;  // owner: the largest lane i with excl_i <= q
+#pragma unroll
+      for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t pv = __shfl_sync(kFull, excl, i + step);
+        if (pv <= q) i += step;
+      }
+      const uint64_t obm = __shfl_sync(kFull, bm, i);
+      of[k] = __shfl_sync(kFull, sflag, i);
+      oo[k] = 0;
+      if constexpr (MODE != AotMode::count) oo[k] = __shfl_sync(kFull, b_orig, i);
+      x[k] = q < total ? __ldg(P.col + obm + q) : kEmpty;
     }
-    const uint64_t obm = __shfl_sync(kFull, bm, i);
-    const uint32_t oflag = __shfl_sync(kFull, sflag, i);
-    uint32_t oorig = 0;
-    if constexpr (MODE != AotMode::count) oorig = __shfl_sync(kFull, b_orig, i);
-    const uint32_t x = q < total ? __ldg(P.col + obm + q) : kEmpty;
-    const uint32_t hit = Probe::kRangeChecked ? probe.bit(x) : uint32_t(x <= lmax && probe.test(x));
-    if (oflag & kNegBit) st.neg += hit; else st.pos += hit;
-    if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oorig, x);
+#pragma unroll
+    for (int k = 0; k < kSU; ++k) {
+      const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
+      if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
+      if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oo[k], x[k]);
+    }
   }
 
   // ---- long claims: the whole warp sweeps one list, kUnroll rounds of 32
