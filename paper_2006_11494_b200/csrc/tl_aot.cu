@@ -41,8 +41,17 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range load
 
 // Tuning knobs (compile-time; see tools/sweep.py):
+// Rounds of 32 traversal loads in flight per warp: 4 for graphs whose mean
+// window is short (L2-resident C2, C3), 6 for long windows (C4, C5), chosen
+// per run from the mean window length.
 #ifndef TL_UNROLL
-#define TL_UNROLL 4  // rounds of 32 traversal loads in flight per warp
+#define TL_UNROLL 4
+#endif
+#ifndef TL_UNROLL_LONG
+#define TL_UNROLL_LONG 6
+#endif
+#ifndef TL_LONG_WINDOW
+#define TL_LONG_WINDOW 160
 #endif
 #ifndef TL_WARP_WORDS
 #define TL_WARP_WORDS 1280  // per-warp probe region in 32-bit words (5 KB: a 40,960-bit span)
@@ -53,7 +62,8 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #ifndef TL_CTA_MIN_WORK
 #define TL_CTA_MIN_WORK 65536
 #endif
-constexpr int kUnroll = TL_UNROLL;
+constexpr int kUnrollShort = TL_UNROLL;
+constexpr int kUnrollLong = TL_UNROLL_LONG;
 #ifndef TL_WARP_CTA_THREADS
 #define TL_WARP_CTA_THREADS 256
 #endif
@@ -270,7 +280,7 @@ __device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, 
 // ------------------------------------------------------------ claim batch
 // One warp processes claims [base, min(base + 32, ce)) of a pivot against the
 // staged probe side.  All 32 lanes must call it.
-template <AotMode MODE, typename Probe>
+template <AotMode MODE, int U, typename Probe>
 __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe, uint32_t lmax, uint32_t a_orig,
                                             uint64_t base, uint64_t ce, Lane<MODE>& st) {
   const uint32_t lane = lane_id();
@@ -330,7 +340,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     }
   }
 
-  // ---- long claims: the whole warp sweeps one list, kUnroll rounds of 32
+  // ---- long claims: the whole warp sweeps one list, U rounds of 32
   // loads in flight; lists are rank-ascending, so a list is abandoned once a
   // group reaches past max N+(l)
   unsigned longm = __ballot_sync(kFull, len > kShort);
@@ -345,20 +355,20 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     const uint32_t* p = P.col + bj + lane;
     int rem = int(lj) - int(lane);  // this lane reads p[32k] while 32k < rem
     uint32_t hits = 0;
-    for (uint32_t r0 = 0; r0 < lj; r0 += 32 * kUnroll) {
-      uint32_t x[kUnroll];
+    for (uint32_t r0 = 0; r0 < lj; r0 += 32 * U) {
+      uint32_t x[U];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+      for (int k = 0; k < U; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
       bool over = false;
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
+      for (int k = 0; k < U; ++k) {
         over |= x[k] > lmax;
         const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
         hits += hit;
         if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oj, x[k]);
       }
-      p += 32 * kUnroll;
-      rem -= 32 * kUnroll;
+      p += 32 * U;
+      rem -= 32 * U;
       if (__any_sync(kFull, over)) break;
     }
     if (nj) st.neg += hits; else st.pos += hits;
@@ -385,7 +395,7 @@ __device__ __forceinline__ void reduce_and_flush(Lane<MODE>& st, const Params& P
 }
 
 // ------------------------------------------------------------ warp kernel
-template <AotMode MODE>
+template <AotMode MODE, int U>
 __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint32_t wbase, Lane<MODE>& st) {
   const uint32_t lane = lane_id();
   const uint32_t* nl = P.col + R.lb;
@@ -397,7 +407,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
     for (uint32_t i = lane; i < R.dl; i += 32) bitmap_set(wbase, lmin, __ldg(nl + i));
     __syncwarp();
     const BitmapProbe probe{wbase, lmin, span};
-    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
     __syncwarp();
     const uint32_t nwords = (span + 31) >> 5;
     if (nwords <= max(64u, 2 * R.dl))
@@ -411,7 +421,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
     for (uint32_t i = lane; i < R.dl; i += 32) hash_insert(wbase, cap - 1, 32 - lg, __ldg(nl + i));
     __syncwarp();
     const HashProbe probe{wbase, cap - 1, 32 - lg};
-    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
     __syncwarp();
     for (uint32_t i = lane; i < cap; i += 32) st_sm(wbase + 4 * i, 0u);
   }
@@ -424,25 +434,38 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
 // on big pivots) one at a time and probes them with all its warps against one
 // probe side built in the union of the warps' regions.  Phase 2: every warp
 // independently takes cost-balanced tasks of records with its own region.
-template <AotMode MODE, typename Probe>
-__device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
-                                           uint32_t a_orig, Lane<MODE>& st) {
-  const uint32_t warp = threadIdx.x >> 5;
-  for (uint64_t base = R.cb + 32 * warp; base < R.ce; base += 32 * kWarpsPerCta)
-    claim_batch<MODE>(P, probe, lmax, a_orig, base, R.ce, st);
+// The CTA's warps take the record's claim batches dynamically from a shared
+// cursor, so the barrier closing the record waits for at most one batch.
+__device__ unsigned long long* cta_cursor() {
+  __shared__ unsigned long long cursor;
+  return &cursor;
 }
 
-template <AotMode MODE>
+template <AotMode MODE, int U, typename Probe>
+__device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
+                                           uint32_t a_orig, Lane<MODE>& st) {
+  unsigned long long* cur = cta_cursor();
+  while (true) {
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(cur, 32ull);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= R.ce) break;
+    claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+  }
+}
+
+template <AotMode MODE, int U>
 __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32_t cbase, Lane<MODE>& st) {
   const uint32_t* nl = P.col + R.lb;
   const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
   const uint32_t span = lmax - lmin + 1;
   uint32_t a_orig = 0;
   if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+  if (threadIdx.x == 0) *cta_cursor() = R.cb;  // published by the barrier after the build
   if (span <= kCtaSpanMax) {
     for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) bitmap_set(cbase, lmin, __ldg(nl + i));
     __syncthreads();
-    cta_claims(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
+    cta_claims<MODE, U>(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
     __syncthreads();
     const uint32_t nwords = (span + 31) >> 5;
     if (nwords <= max(uint32_t(kWarpThreads), 2 * R.dl))
@@ -455,16 +478,17 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
     const uint32_t cap = 1u << lg;
     for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
     __syncthreads();
-    cta_claims(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
+    cta_claims<MODE, U>(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < cap; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
   } else {
-    cta_claims(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
+    __syncthreads();
+    cta_claims<MODE, U>(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
   }
   st.fold();
 }
 
-template <AotMode MODE>
+template <AotMode MODE, int U>
 __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS_PER_SM : 3) k_aot(Params P) {
   __shared__ unsigned long long s_task;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -482,7 +506,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS
       const unsigned long long t = s_task;
       __syncthreads();
       if (t >= P.ncta) break;
-      cta_record(P, P.crecs[t], cbase, st);
+      cta_record<MODE, U>(P, P.crecs[t], cbase, st);
     }
   }
   // ---- phase 2: warp tasks
@@ -492,7 +516,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS
     t = __shfl_sync(kFull, t, 0);
     if (t >= P.ntasks) break;
     const uint2 tk = P.tasks[P.ntasks - 1 - t];  // heaviest pivots (highest ranks) first
-    for (uint32_t r = tk.x; r < tk.y; ++r) warp_record(P, P.recs[r], wbase, st);
+    for (uint32_t r = tk.x; r < tk.y; ++r) warp_record<MODE, U>(P, P.recs[r], wbase, st);
   }
   reduce_and_flush(st, P);
 }
@@ -711,26 +735,33 @@ size_t kernel_smem() {
 }
 
 template <AotMode MODE>
-int resident_warps() {  // warps of k_aot<MODE> the current device keeps resident (cached per device)
+int resident_warps() {  // warps of k_aot<MODE, *> the current device keeps resident (cached per device)
   static int cache[64] = {0};
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
   if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
-  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kernel_smem<MODE>())));
+  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE, kUnrollShort>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kernel_smem<MODE>())));
+  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE, kUnrollLong>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kernel_smem<MODE>())));
   int per_sm = 0;
-  TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot<MODE>, kWarpThreads, kernel_smem<MODE>()));
+  TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot<MODE, kUnrollShort>, kWarpThreads,
+                                                        kernel_smem<MODE>()));
   const int w = sm_count() * std::max(per_sm, 1) * kWarpsPerCta;
   if (dev >= 0 && dev < 64) cache[dev] = w;
   return w;
 }
 
 template <AotMode MODE>
-uint64_t launch_kernels(const Params& P, cudaStream_t s) {
+uint64_t launch_kernels(const Params& P, bool long_lists, cudaStream_t s) {
   if (!P.ntasks && !P.ncta) return 0;
   const uint64_t ctas = uint64_t(resident_warps<MODE>()) / kWarpsPerCta;
   const uint64_t want = std::max<uint64_t>(P.ncta, (P.ntasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const unsigned grid = unsigned(std::min<uint64_t>(want, ctas));
-  k_aot<MODE><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
+  if (long_lists)
+    k_aot<MODE, kUnrollLong><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
+  else
+    k_aot<MODE, kUnrollShort><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
   TL_CUDA(cudaGetLastError());
   return 1;
 }
@@ -796,6 +827,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
 
   // adaptive task size: ~64 warp tasks per resident warp
   uint64_t T = kTaskMin;
+  bool long_lists = false;
   {
     uint64_t w[2] = {0, 0};
     TL_CUDA(cudaMemcpyAsync(w, CP.p + cb, 8, cudaMemcpyDeviceToHost, s));
@@ -809,6 +841,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
       case AotMode::list: warps = resident_warps<AotMode::list>(); break;
     }
     T = std::max<uint64_t>(kTaskMin, work / (uint64_t(std::max(warps, 1)) * 64));
+    long_lists = ce > cb && (w[1] - w[0]) / (ce - cb) >= TL_LONG_WINDOW;
   }
 
   const uint32_t np = cb < ce ? pe - pb : 0;
@@ -893,9 +926,9 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   P.crecs = crecs.p;
   P.ncta = nc;
   switch (mode) {
-    case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, s); break;
-    case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, s); break;
-    case AotMode::list: r.launches += launch_kernels<AotMode::list>(P, s); break;
+    case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, long_lists, s); break;
+    case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, long_lists, s); break;
+    case AotMode::list: r.launches += launch_kernels<AotMode::list>(P, long_lists, s); break;
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];
