@@ -437,7 +437,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "bytes_per_launch": B["count"] // world, "peak_source": peaks["source"],
-                         "kernel": "k_aot_warp + k_aot_cta (AOT intersection), CUDA events on the launch stream"},
+                         "kernel": "k_aot (AOT intersection, both phases), CUDA events on the launch stream"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "list": list_info,
