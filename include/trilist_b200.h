@@ -31,6 +31,9 @@ extern "C" {
 #define TL_ENOMEM 5
 #define TL_ECAPACITY 6
 #define TL_ENODEV 7
+#define TL_EPARSE 8   /* ParseError (graph.hpp:89-96): the message starts with "line N: " */
+#define TL_ELENGTH 9  /* std::length_error                                            */
+#define TL_EIO 10     /* std::runtime_error (cannot open / read a file)              */
 
 #define TL_API __attribute__((visibility("default")))
 
@@ -93,6 +96,26 @@ TL_API int tl_graph_info(const tl_graph* g, uint32_t* n, uint64_t* m, uint64_t* 
 TL_API int tl_graph_degrees(tl_graph* g, uint32_t* degrees);
 /* offsets() (n+1) / adjacency() (2m): symmetric ascending CSR (graph.hpp:56-57). */
 TL_API int tl_graph_csr(tl_graph* g, uint64_t* offsets, uint32_t* adjacency);
+
+/* Edge-list ingestion -- load_edge_list_text / load_edge_list / load_edge_list_file
+ * (graph.hpp:99-108, graph.cpp:40-146, :240-275): whitespace-separated id pairs,
+ * lines starting with a comment prefix skipped, parsed on the device, then
+ * Graph::from_edges on the device.  On a ParseError the call returns TL_EPARSE
+ * and *error_line holds the 1-based line (the first bad line, as the
+ * reference reports it). */
+#define TL_LOAD_ONE_INDEXED 1u /* LoadOptions::one_indexed */
+#define TL_LOAD_COMPACT_IDS 2u /* LoadOptions::compact_ids */
+typedef struct tl_load_diag {  /* LoadDiagnostics (graph.hpp:81-86) */
+  uint64_t lines_read;
+  uint64_t edges_parsed;
+  uint64_t self_loops_dropped;
+  uint64_t duplicates_dropped;
+} tl_load_diag;
+TL_API int tl_graph_from_text(const char* text, uint64_t len, uint32_t flags, const char* comment_prefixes,
+                              int device, tl_graph** out, tl_load_diag* diag, uint64_t* error_line);
+/* gzip-transparent; path "-" reads stdin. */
+TL_API int tl_graph_from_file(const char* path, uint32_t flags, const char* comment_prefixes, int device,
+                              tl_graph** out, tl_load_diag* diag, uint64_t* error_line);
 
 /* ---------------------------------------------------------- L1 ordering */
 /* degree_order(const Graph&) -- ordering.hpp:24, ordering.cpp:69-84: rank[u] by

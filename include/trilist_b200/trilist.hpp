@@ -19,6 +19,8 @@
 #include <compare>
 #include <cstdint>
 #include <initializer_list>
+#include <iosfwd>
+#include <string_view>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -76,6 +78,7 @@ class Graph {
   std::uint64_t self_loops_dropped() const { return loops_; }
   tl_graph* handle() const { return h_.get(); }
   int device() const { return device_; }
+  static Graph adopt(tl_graph* h, int device) { return wrap(h, device); }  // takes ownership
 
  private:
   struct HostCsr {
@@ -92,6 +95,43 @@ class Graph {
   std::uint64_t dups_ = 0, loops_ = 0;
   mutable std::shared_ptr<HostCsr> csr_;
 };
+
+// --------------------------------------------------- graph.hpp: loading
+struct LoadOptions {
+  std::string comment_prefixes = "#%";  // line-leading chars that mark comments
+  bool one_indexed = false;             // input numbers vertices from 1
+  bool compact_ids = false;             // remap ids to 0..n-1 by first appearance
+};
+
+struct LoadDiagnostics {
+  std::uint64_t lines_read = 0;
+  std::uint64_t edges_parsed = 0;  // pairs seen, before normalization
+  std::uint64_t self_loops_dropped = 0;
+  std::uint64_t duplicates_dropped = 0;
+};
+
+struct LoadResult {
+  Graph graph;
+  LoadDiagnostics diagnostics;
+};
+
+/// Input rejection with the 1-based line it occurred on (graph.hpp:89-96).
+class ParseError : public std::runtime_error {
+ public:
+  ParseError(const std::string& what, std::uint64_t line) : std::runtime_error(what), line_(line) {}
+  std::uint64_t line() const { return line_; }
+
+ private:
+  std::uint64_t line_;
+};
+
+/// Parsed on the device (tl_graph_from_text / tl_graph_from_file).
+LoadResult load_edge_list(std::istream& in, const LoadOptions& options = {});
+LoadResult load_edge_list_text(std::string_view text, const LoadOptions& options = {});
+/// gzip-transparent; "-" reads stdin.
+LoadResult load_edge_list_file(const std::string& path, const LoadOptions& options = {});
+/// Writes each undirected edge once, smaller endpoint first, ascending.
+void write_edge_list(const Graph& g, std::ostream& out);
 
 // ---------------------------------------------------------- ordering.hpp
 struct VertexOrder {

@@ -352,6 +352,10 @@ def rlib() -> C.CDLL:
     L.ref_brute_force.argtypes = [C.c_void_p, C.c_uint32, u32p, C.c_uint64, u64p]
     L.ref_download_oriented.argtypes = [C.c_void_p, u64p, u32p, u64p, u32p, u32p]
     L.ref_download_graph.argtypes = [C.c_void_p, u64p, u32p]
+    L.ref_load_text.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p), u64p,
+                                u64p]
+    L.ref_write_edge_list.restype = C.c_uint64
+    L.ref_write_edge_list.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
     return L
 
 
@@ -364,8 +368,42 @@ def hardware_threads() -> int:
     return int(rlib().ref_hardware_threads())
 
 
+class RefParseError(ValueError):
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
 class RefGraph:
     """Graph::from_edges -> make_order -> orient, by the reference library."""
+
+    @classmethod
+    def from_text(cls, text: bytes, one_indexed=False, compact=False, comments="#%"):
+        """load_edge_list_text (graph.cpp:240-248) + degree order + orient.
+        Returns (RefGraph, diagnostics dict); raises RefParseError."""
+        if isinstance(text, str):
+            text = text.encode()
+        h = C.c_void_p()
+        diag = np.zeros(4, np.uint64)
+        line = np.zeros(1, np.uint64)
+        rc = rlib().ref_load_text(text, len(text), int(one_indexed), int(compact), comments.encode(), C.byref(h),
+                                  _p64(diag), _p64(line))
+        if rc == 2:
+            raise RefParseError(rlib().ref_last_error().decode(), int(line[0]))
+        _rcheck(rc)
+        self = cls.__new__(cls)
+        self._h = h
+        self.phase_times = {}
+        self.n = rlib().ref_n(h)
+        self.m = rlib().ref_m(h)
+        keys = ("lines_read", "edges_parsed", "self_loops_dropped", "duplicates_dropped")
+        return self, {k: int(v) for k, v in zip(keys, diag)}
+
+    def write_edge_list(self) -> bytes:
+        size = rlib().ref_write_edge_list(self._h, None, 0)
+        buf = C.create_string_buffer(max(size, 1))
+        rlib().ref_write_edge_list(self._h, buf, size)
+        return buf.raw[:size]
 
     def __init__(self, min_vertices: int, pairs, order: str = "degree", local: str = "rank-asc"):
         pairs = np.ascontiguousarray(as_pairs(pairs) if not isinstance(pairs, np.ndarray) else pairs,

@@ -18,6 +18,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <sstream>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -224,6 +226,45 @@ int ref_download_oriented(void* hp, std::uint64_t* out_off, std::uint32_t* out, 
     if (out_off) out_off[og.num_vertices()] = pos_out;
     if (in_off) in_off[og.num_vertices()] = pos_in;
   });
+}
+
+// load_edge_list_text (graph.cpp:240-248) then degree order + orient.
+// Returns 0, 1 (other error) or 2 (ParseError; *err_line set).
+// diag[4] = lines_read, edges_parsed, self_loops_dropped, duplicates_dropped.
+int ref_load_text(const char* text, std::uint64_t len, int one_indexed, int compact, const char* comments,
+                  void** out, std::uint64_t* diag, std::uint64_t* err_line) {
+  try {
+    LoadOptions opt;
+    opt.one_indexed = one_indexed != 0;
+    opt.compact_ids = compact != 0;
+    if (comments) opt.comment_prefixes = comments;
+    LoadResult r = load_edge_list_text(std::string_view(text, len), opt);
+    auto* h = new Handle;
+    h->g = std::move(r.graph);
+    h->og = orient(h->g, degree_order(h->g));
+    diag[0] = r.diagnostics.lines_read;
+    diag[1] = r.diagnostics.edges_parsed;
+    diag[2] = r.diagnostics.self_loops_dropped;
+    diag[3] = r.diagnostics.duplicates_dropped;
+    *out = h;
+    return 0;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    *err_line = e.line();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// write_edge_list (graph.cpp:277-281) into a caller buffer; returns the size.
+std::uint64_t ref_write_edge_list(void* hp, char* buf, std::uint64_t cap) {
+  std::ostringstream os;
+  write_edge_list(static_cast<Handle*>(hp)->g, os);
+  std::string s = os.str();
+  if (buf) std::memcpy(buf, s.data(), std::min<std::uint64_t>(cap, s.size()));
+  return s.size();
 }
 
 int ref_download_graph(void* hp, std::uint64_t* off, std::uint32_t* adj) {

@@ -16,14 +16,15 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TL_LIB_PATH") or os.path.join(PKG, "lib", "libtrilist_b200.so")
 
-TL_OK, TL_EINVAL, TL_ERANGE, TL_ELOGIC, TL_ECUDA, TL_ENOMEM, TL_ECAPACITY, TL_ENODEV = range(8)
+(TL_OK, TL_EINVAL, TL_ERANGE, TL_ELOGIC, TL_ECUDA, TL_ENOMEM, TL_ECAPACITY, TL_ENODEV, TL_EPARSE, TL_ELENGTH,
+ TL_EIO) = range(11)
 
 # Every symbol include/trilist_b200.h declares (checked by tests/test_cabi_symbols.py).
 EXPORTS = (
     "tl_last_error", "tl_device_count", "tl_version",
     "tl_gen_er", "tl_gen_rmat", "tl_chung_lu_prefix", "tl_gen_chung_lu",
     "tl_graph_from_pairs", "tl_graph_free", "tl_graph_info", "tl_graph_degrees", "tl_graph_csr",
-    "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
+    "tl_graph_from_text", "tl_graph_from_file", "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
     "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list", "tl_brute_force",
 )
 
@@ -40,6 +41,14 @@ class TlStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class TlLoadDiag(C.Structure):
+    _fields_ = [("lines_read", C.c_uint64), ("edges_parsed", C.c_uint64), ("self_loops_dropped", C.c_uint64),
+                ("duplicates_dropped", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class TlRunOptions(C.Structure):
     _fields_ = [("skip_negative_phase", C.c_uint32), ("check_hygiene", C.c_uint32), ("part", C.c_uint32),
                 ("nparts", C.c_uint32), ("stream", C.c_void_p)]
@@ -49,6 +58,12 @@ class TlError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[TL error {code}] {msg}")
         self.code = code
+
+
+class TlParseError(TlError, ValueError):
+    def __init__(self, msg: str, line: int):
+        TlError.__init__(self, TL_EPARSE, msg)
+        self.line = line
 
 
 u32p = C.POINTER(C.c_uint32)
@@ -69,6 +84,10 @@ def lib() -> C.CDLL:
     L.tl_chung_lu_prefix.argtypes = [C.c_uint64, C.c_uint32, C.c_double, C.c_double, u64p]
     L.tl_gen_chung_lu.argtypes = [C.c_uint64, C.c_uint32, u64p, C.c_uint64, vp, vp]
     L.tl_graph_from_pairs.argtypes = [vp, C.c_uint64, C.c_uint32, C.c_int, C.c_int, vp, C.POINTER(vp)]
+    L.tl_graph_from_text.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.c_char_p, C.c_int, C.POINTER(vp),
+                                     C.POINTER(TlLoadDiag), u64p]
+    L.tl_graph_from_file.argtypes = [C.c_char_p, C.c_uint32, C.c_char_p, C.c_int, C.POINTER(vp),
+                                     C.POINTER(TlLoadDiag), u64p]
     L.tl_graph_free.argtypes = [vp]
     L.tl_graph_info.argtypes = [vp, u32p, u64p, u64p, u64p]
     L.tl_graph_degrees.argtypes = [vp, u32p]
@@ -148,6 +167,31 @@ class DeviceGraph:
         _check(lib().tl_graph_from_pairs(pairs.ctypes.data if pairs.size else None, pairs.shape[0], min_vertices,
                                          device, 0, None, C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def from_text(cls, text, one_indexed=False, compact_ids=False, comments="#%", device=0):
+        """load_edge_list_text on the device: returns (DeviceGraph, diagnostics)."""
+        if isinstance(text, str):
+            text = text.encode()
+        h, diag, line = vp(), TlLoadDiag(), C.c_uint64()
+        flags = (1 if one_indexed else 0) | (2 if compact_ids else 0)
+        rc = lib().tl_graph_from_text(text, len(text), flags, comments.encode(), device, C.byref(h), C.byref(diag),
+                                      C.byref(line))
+        if rc == TL_EPARSE:
+            raise TlParseError(lib().tl_last_error().decode(), line.value)
+        _check(rc)
+        return cls(h), diag.as_dict()
+
+    @classmethod
+    def from_file(cls, path, one_indexed=False, compact_ids=False, comments="#%", device=0):
+        h, diag, line = vp(), TlLoadDiag(), C.c_uint64()
+        flags = (1 if one_indexed else 0) | (2 if compact_ids else 0)
+        rc = lib().tl_graph_from_file(str(path).encode(), flags, comments.encode(), device, C.byref(h),
+                                      C.byref(diag), C.byref(line))
+        if rc == TL_EPARSE:
+            raise TlParseError(lib().tl_last_error().decode(), line.value)
+        _check(rc)
+        return cls(h), diag.as_dict()
 
     @classmethod
     def from_device_pairs(cls, d_ptr: int, npairs: int, min_vertices: int, device: int = 0,

@@ -8,7 +8,11 @@
 #include <algorithm>
 #include <charconv>
 #include <cstring>
+#include <istream>
+#include <iterator>
 #include <mutex>
+#include <ostream>
+#include <sstream>
 
 namespace trilist {
 
@@ -110,6 +114,66 @@ bool Graph::validate(std::string* why) const {  // graph.cpp:219-238
     }
   }
   return true;
+}
+
+// ----------------------------------------------------------------- loading
+namespace {
+LoadResult load_common(int rc, tl_graph* h, const tl_load_diag& d, std::uint64_t line) {
+  if (rc == TL_EPARSE) throw ParseError(tl_last_error(), line);
+  if (rc == TL_ELENGTH) throw std::length_error(tl_last_error());
+  check(rc, "load_edge_list");
+  LoadResult r;
+  r.graph = Graph::adopt(h, 0);
+  r.diagnostics.lines_read = d.lines_read;
+  r.diagnostics.edges_parsed = d.edges_parsed;
+  r.diagnostics.self_loops_dropped = d.self_loops_dropped;
+  r.diagnostics.duplicates_dropped = d.duplicates_dropped;
+  return r;
+}
+
+std::uint32_t load_flags(const LoadOptions& o) {
+  return (o.one_indexed ? TL_LOAD_ONE_INDEXED : 0u) | (o.compact_ids ? TL_LOAD_COMPACT_IDS : 0u);
+}
+}  // namespace
+
+LoadResult load_edge_list_text(std::string_view text, const LoadOptions& options) {  // graph.cpp:244-248
+  tl_graph* h = nullptr;
+  tl_load_diag d{};
+  std::uint64_t line = 0;
+  int rc = tl_graph_from_text(text.data(), text.size(), load_flags(options), options.comment_prefixes.c_str(), 0, &h,
+                              &d, &line);
+  return load_common(rc, h, d, line);
+}
+
+LoadResult load_edge_list(std::istream& in, const LoadOptions& options) {  // graph.cpp:240-242
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return load_edge_list_text(text, options);
+}
+
+LoadResult load_edge_list_file(const std::string& path, const LoadOptions& options) {  // graph.cpp:250-275
+  tl_graph* h = nullptr;
+  tl_load_diag d{};
+  std::uint64_t line = 0;
+  int rc = tl_graph_from_file(path.c_str(), load_flags(options), options.comment_prefixes.c_str(), 0, &h, &d, &line);
+  if (rc == TL_EIO) throw std::runtime_error(tl_last_error());
+  return load_common(rc, h, d, line);
+}
+
+void write_edge_list(const Graph& g, std::ostream& out) {  // graph.cpp:277-281
+  std::string buf;
+  for (VertexId u = 0; u < g.num_vertices(); ++u)
+    for (VertexId v : g.neighbors(u))
+      if (v > u) {
+        buf += std::to_string(u);
+        buf += ' ';
+        buf += std::to_string(v);
+        buf += '\n';
+        if (buf.size() > (1u << 20)) {
+          out << buf;
+          buf.clear();
+        }
+      }
+  out << buf;
 }
 
 // --------------------------------------------------------------- ordering

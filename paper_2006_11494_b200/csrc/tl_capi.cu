@@ -210,6 +210,52 @@ int tl_graph_from_pairs(const uint32_t* pairs, uint64_t npairs, uint32_t min_ver
   });
 }
 
+static int load_common(const char* text, uint64_t len, uint32_t flags, const char* comments, int device,
+                       tl_graph** out, tl_load_diag* diag, uint64_t* error_line, const std::string* owned) {
+  (void)owned;
+  try {
+    TL_REQUIRE(out, TL_EINVAL, "out is NULL");
+    TL_REQUIRE(text || len == 0, TL_EINVAL, "text is NULL");
+    *out = nullptr;
+    if (error_line) *error_line = 0;
+    require_device(device);
+    tlb::DeviceGuard guard(device);
+    tlb::ensure_device_setup(device);
+    auto g = std::make_unique<tl_graph>();
+    g->device = device;
+    TL_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    tlb::graph_from_text(*g, text, len, flags, comments, diag);
+    *out = g.release();
+    return TL_OK;
+  } catch (const tlb::ParseFailure& e) {
+    g_last_error = e.what();
+    if (error_line) *error_line = e.line;
+    return TL_EPARSE;
+  } catch (const tlb::TlError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TL_ECUDA;
+  }
+}
+
+int tl_graph_from_text(const char* text, uint64_t len, uint32_t flags, const char* comment_prefixes, int device,
+                       tl_graph** out, tl_load_diag* diag, uint64_t* error_line) {
+  return load_common(text, len, flags, comment_prefixes, device, out, diag, error_line, nullptr);
+}
+
+int tl_graph_from_file(const char* path, uint32_t flags, const char* comment_prefixes, int device, tl_graph** out,
+                       tl_load_diag* diag, uint64_t* error_line) {
+  std::string text;
+  const int rc = guarded([&] {
+    TL_REQUIRE(path, TL_EINVAL, "path is NULL");
+    text = tlb::read_text_file(path);
+  });
+  if (rc != TL_OK) return rc;
+  return load_common(text.data(), text.size(), flags, comment_prefixes, device, out, diag, error_line, &text);
+}
+
 int tl_graph_free(tl_graph* g) {
   return guarded([&] {
     if (!g) return;

@@ -77,6 +77,15 @@ void gen_chung_lu(uint64_t seed, uint32_t n, const uint64_t* prefix, uint64_t np
 void chung_lu_prefix_host(uint64_t seed, uint32_t n, double avg, double gamma, uint64_t* prefix);
 
 void graph_from_pairs(tl_graph& g, const uint32_t* d_pairs, uint64_t npairs, uint32_t min_vertices);
+
+// ---- tl_parse.cu ----
+struct ParseFailure : TlError {
+  uint64_t line;
+  ParseFailure(uint64_t line_no, const std::string& msg);
+};
+void graph_from_text(tl_graph& g, const char* text, uint64_t len, uint32_t flags, const char* comment_prefixes,
+                     tl_load_diag* diag);
+std::string read_text_file(const std::string& path);
 void graph_csr(tl_graph& g, DBuf<uint64_t>& off, DBuf<uint32_t>& adj);
 void degree_order(tl_graph& g, DBuf<uint32_t>& rank);  // device rank[n]
 void orient(tl_graph& g, const uint32_t* d_rank, tl_oriented& og);
