@@ -40,12 +40,19 @@ extern "C" {
 typedef struct tl_graph tl_graph;       /* device-resident Graph (graph.hpp:31-73)            */
 typedef struct tl_oriented tl_oriented; /* device-resident OrientedGraph (ordering.hpp:62-108) */
 
-/* RunStats (engine.hpp:28-54) plus device-side extras. */
+/* The reference's kernels (Algorithm, engine.hpp:18; names engine.cpp:7-15). */
+#define TL_ALGO_AOT 0      /* "aot"     aot_pivot      engine.hpp:238-276 */
+#define TL_ALGO_CF_MERGE 1 /* "cf"      cf_merge_pivot engine.hpp:164-184 */
+#define TL_ALGO_CF_HASH 2  /* "cf-hash" cf_hash_pivot  engine.hpp:186-215 */
+#define TL_ALGO_KCLIST3 3  /* "kclist"  kclist3_pivot  engine.hpp:217-236 */
+
+/* RunStats (engine.hpp:28-54) plus device-side extras.  The six reference
+ * counters are exactly what the reference kernel of the run's algorithm keeps. */
 typedef struct tl_stats {
   uint64_t triangles;
-  uint64_t probes;            /* logical probes: sum of deg+ of every traversed list (== aot_cost) */
-  uint64_t merge_comparisons; /* always 0 for aot                                                  */
-  uint64_t table_builds;      /* sum of deg+ over all pivots (== m)                                */
+  uint64_t probes;            /* aot, cf-hash: sum of min(deg+) (aot_cost); kclist: kclist_cost; cf: 0 */
+  uint64_t merge_comparisons; /* cf only: iterations of the merge loops                                */
+  uint64_t table_builds;      /* aot, kclist: m; cf-hash: probe-set insertions; cf: 0                 */
   uint64_t positive_triangles;
   uint64_t negative_triangles;
   uint64_t probes_executed;   /* probes left after rank-window early exit                          */
@@ -64,6 +71,8 @@ typedef struct tl_run_options {
   uint32_t part;                /* this device's share of the cost-balanced edge partition          */
   uint32_t nparts;              /* number of shares (GPUs); 0 or 1 = whole graph                    */
   void* stream;                 /* cudaStream_t to run on; NULL = the handle's own stream           */
+  uint32_t algorithm;           /* TL_ALGO_* for tl_run_*; 0 (aot) when zero-initialised            */
+  uint32_t cf_hash_reuse_last_table; /* RunOptions::cf_hash_reuse_last_table (engine.hpp:58)      */
 } tl_run_options;
 
 /* ---------------------------------------------------------------- runtime */
@@ -157,6 +166,27 @@ TL_API int tl_aot_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* sta
  * least the emission count (TL_ECAPACITY otherwise; stats are still filled). */
 TL_API int tl_aot_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
                        int canonical, tl_stats* stats);
+
+/* --------------------------------------------- L2/L3 any kernel by name */
+/* run_counting / run_collecting / run_parallel_count / run_parallel_collecting
+ * for Algorithm = opt->algorithm (engine.hpp:324-329, parallel.hpp:81-88).
+ * Same contracts as tl_aot_count / tl_aot_hash / tl_aot_list; emission role
+ * order is the kernel's own (pivot, neighbor, witness): kclist and cf emit
+ * (u, v, w) for the edge u->v, cf-hash (u, v, w) for the edge u->v whichever
+ * side it hashed (engine.hpp:212).  tl_aot_* ignore opt->algorithm. */
+TL_API int tl_run_count(tl_oriented* og, const tl_run_options* opt, tl_stats* stats);
+TL_API int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats);
+TL_API int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
+                       int canonical, tl_stats* stats);
+
+/* degeneracy_order / random_order -- ordering.cpp:86-120.  The degeneracy
+ * order removes, one vertex at a time, the vertex of least (current degree,
+ * id) -- an inherently sequential chain -- and random_order is a Fisher-Yates
+ * chain of n dependent swaps; both run on the host (O(m log n) / O(n)) over
+ * the graph's CSR and return rank[n] for tl_orient.  Not on the AOT path,
+ * which uses the device degree order. */
+TL_API int tl_degeneracy_order(tl_graph* g, uint32_t* rank);
+TL_API int tl_random_order(uint32_t n, uint64_t seed, uint32_t* rank);
 
 /* brute_force_triangles(const Graph&, OracleOptions) -- oracle.hpp:18, oracle.cpp:8-25,
  * as a device kernel: sorted canonical set.  TL_EINVAL if n > max_vertices. */

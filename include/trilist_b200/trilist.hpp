@@ -5,11 +5,13 @@
 // /root/reference/proj/include/trilist); every computation runs through
 // include/trilist_b200.h on a CUDA device.  Differences, all documented in
 // INTEGRATION.md:
-//   * Algorithm::aot is the only kernel on the B200 path; the others throw
-//     std::invalid_argument (no CPU fallback).
-//   * OrderKind::degeneracy / random throw std::invalid_argument (the north
-//     star fixes the degree order); any explicit VertexOrder permutation is
-//     accepted by orient().
+//   * all four kernels (aot, cf, cf-hash, kclist) run on the device with the
+//     reference's exact counters; the device keeps rank-ascending lists, and
+//     other local orders are host-side views (counters are layout-invariant,
+//     test_engine.cpp:172-185; cf still rejects non-rank-ascending layouts).
+//   * the degeneracy and random orders are sequential chains by definition
+//     and are computed on the host (tl_degeneracy_order / tl_random_order);
+//     the degree order and everything after it run on the device.
 //   * ParallelConfig is validated exactly like the reference (workers >= 1,
 //     chunk >= 1) but no longer partitions work: the GPU schedules its own
 //     cost-balanced tasks.
@@ -142,8 +144,8 @@ struct VertexOrder {
 
 VertexOrder id_order(const Graph& g);
 VertexOrder degree_order(const Graph& g);  // device counting order, ordering.cpp:69-84
-VertexOrder degeneracy_order(const Graph& g);  // std::invalid_argument on this path
-VertexOrder random_order(const Graph& g, std::uint64_t seed);  // std::invalid_argument on this path
+VertexOrder degeneracy_order(const Graph& g);  // sequential chain: host (tl_degeneracy_order), ordering.cpp:86-114
+VertexOrder random_order(const Graph& g, std::uint64_t seed);  // Fisher-Yates chain: host (tl_random_order)
 
 enum class OrderKind { id, degree, degeneracy, random };
 struct OrderSpec {
@@ -223,8 +225,8 @@ EdgePolarity edge_polarity(const OrientedGraph& g, VertexId u, VertexId v);
 enum class Algorithm { cf_merge, cf_hash, kclist3, aot };
 inline constexpr std::array<Algorithm, 4> kAllAlgorithms = {Algorithm::cf_merge, Algorithm::cf_hash,
                                                             Algorithm::kclist3, Algorithm::aot};
-/// Algorithms with a B200 implementation.
-inline constexpr std::array<Algorithm, 1> kDeviceAlgorithms = {Algorithm::aot};
+/// Algorithms with a B200 implementation (all of them).
+inline constexpr std::array<Algorithm, 4> kDeviceAlgorithms = kAllAlgorithms;
 const char* to_string(Algorithm a);
 Algorithm parse_algorithm(const std::string& name);
 
@@ -258,7 +260,7 @@ struct RunStats {
 
 struct RunOptions {
   bool check_bitmap_between_pivots = false;  // accepted; the device tables are per work item
-  bool cf_hash_reuse_last_table = false;     // cf-hash only (not on this path)
+  bool cf_hash_reuse_last_table = false;     // skip rebuild if same owner, pivot-scoped
   bool aot_skip_negative_phase = false;      // fault injection hook for the verifier
 };
 
@@ -272,23 +274,37 @@ struct CollectingSink {
 
 namespace detail {
 void require_device_algorithm(Algorithm a);
-RunStats device_count(const OrientedGraph& g, const RunOptions& opt, int mode /*0 count, 1 hash*/);
-RunStats device_list(const OrientedGraph& g, const RunOptions& opt, std::vector<std::array<VertexId, 3>>& raw);
+std::uint32_t algorithm_code(Algorithm a);                    // TL_ALGO_*
+void assert_layout(Algorithm a, const OrientedGraph& g);      // cf: rank-ascending lists (engine.hpp:143-149)
+RunStats device_count(Algorithm algo, const OrientedGraph& g, const RunOptions& opt, int mode /*0 count, 1 hash*/);
+RunStats device_list(Algorithm algo, const OrientedGraph& g, const RunOptions& opt,
+                     std::vector<std::array<VertexId, 3>>& raw);
 }  // namespace detail
 
 template <typename Sink>
 RunStats run_algorithm(Algorithm algo, const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
-  detail::require_device_algorithm(algo);
   if constexpr (std::is_same_v<std::decay_t<Sink>, NullSink>) {
-    return detail::device_count(g, opt, 0);
+    return detail::device_count(algo, g, opt, 0);
   } else {
     std::vector<std::array<VertexId, 3>> raw;
-    RunStats s = detail::device_list(g, opt, raw);
+    RunStats s = detail::device_list(algo, g, opt, raw);
     for (const auto& t : raw) sink(t[0], t[1], t[2]);  // role order (pivot, neighbor, witness)
     return s;
   }
 }
 
+template <typename Sink>
+RunStats cf_merge(const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
+  return run_algorithm(Algorithm::cf_merge, g, sink, opt);
+}
+template <typename Sink>
+RunStats cf_hash(const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
+  return run_algorithm(Algorithm::cf_hash, g, sink, opt);
+}
+template <typename Sink>
+RunStats kclist3(const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
+  return run_algorithm(Algorithm::kclist3, g, sink, opt);
+}
 template <typename Sink>
 RunStats aot(const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
   return run_algorithm(Algorithm::aot, g, sink, opt);

@@ -91,6 +91,11 @@ def olib() -> C.CDLL:
     L.or_aot.argtypes = [C.c_void_p, C.c_int, u64p, u32p, C.c_uint64]
     L.or_brute_force.restype = C.c_uint64
     L.or_brute_force.argtypes = [C.c_void_p, u32p, C.c_uint64]
+    L.or_kernel.restype = C.c_uint64
+    L.or_kernel.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, u32p, C.c_uint64]
+    L.or_apply_local_order.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
+    L.or_degeneracy_order.argtypes = [C.c_void_p, u32p]
+    L.or_random_order.argtypes = [C.c_uint32, C.c_uint64, u32p]
     return L
 
 
@@ -236,6 +241,28 @@ class OracleGraph:
         olib().or_degree_order(self._h, _p32(rank))
         return rank[: self.n]
 
+    def degeneracy_order(self) -> np.ndarray:
+        rank = np.empty(max(self.n, 1), np.uint32)
+        olib().or_degeneracy_order(self._h, _p32(rank))
+        return rank[: self.n]
+
+    def random_order(self, seed: int) -> np.ndarray:
+        rank = np.empty(max(self.n, 1), np.uint32)
+        olib().or_random_order(self.n, seed, _p32(rank))
+        return rank[: self.n]
+
+    def make_order(self, spec: str) -> np.ndarray:
+        """make_order(parse_order_spec(spec)) -- ordering.cpp:122-141."""
+        if spec == "id":
+            return np.arange(self.n, dtype=np.uint32)
+        if spec == "degree":
+            return self.degree_order()
+        if spec == "degeneracy":
+            return self.degeneracy_order()
+        if spec.startswith("random:"):
+            return self.random_order(int(spec[7:]))
+        raise ValueError(f"unknown order '{spec}'")
+
     def orient(self, rank=None) -> "OracleOriented":
         rank = self.degree_order() if rank is None else np.ascontiguousarray(rank, np.uint32)
         h = olib().or_orient(self._h, _p32(rank))
@@ -297,6 +324,35 @@ class OracleOriented:
         return d, raw
 
 
+    def apply_local_order(self, spec: str) -> None:
+        """Rewrites the out-lists in place (ordering.cpp:229-266)."""
+        if spec == "rank-asc":
+            olib().or_apply_local_order(self._h, 0, 0)
+        elif spec == "degree-desc":
+            olib().or_apply_local_order(self._h, 1, 0)
+        elif spec.startswith("random:"):
+            olib().or_apply_local_order(self._h, 2, int(spec[7:]))
+        else:
+            raise ValueError(f"unknown local order '{spec}'")
+
+    def run(self, algo: str, reuse=False, skip_negative=False, collect=False):
+        """Any of the reference's four kernels (engine.hpp:164-304) by name."""
+        if algo == "aot":
+            return self.aot(skip_negative=skip_negative, collect=collect)
+        code = {"cf": 0, "cf-hash": 1, "kclist": 2}[algo]
+        st = np.zeros(8, np.uint64)
+        cnt = olib().or_kernel(self._h, code, int(reuse), _p64(st), None, 0)
+        raw = None
+        if collect:
+            raw = np.empty((max(cnt, 1), 3), np.uint32)
+            olib().or_kernel(self._h, code, int(reuse), _p64(st), _p32(raw), cnt)
+            raw = raw[:cnt]
+        d = {k: int(st[i]) for i, k in enumerate(STAT_KEYS)}
+        d["hash_sum"] = int(st[6])
+        d["hash_xor"] = int(st[7])
+        return d, raw
+
+
 def canonical_sorted(raw: np.ndarray) -> np.ndarray:
     """canonicalize_emissions (engine.cpp:51-57) + unique, on numpy arrays."""
     if raw.size == 0:
@@ -349,6 +405,9 @@ def rlib() -> C.CDLL:
     L.ref_collect.argtypes = [C.c_void_p, C.c_uint, C.c_uint, C.c_int, u32p, C.c_uint64, u64p, u64p,
                               C.POINTER(C.c_double)]
     L.ref_cost_model.argtypes = [C.c_void_p, u64p]
+    L.ref_run.argtypes = [C.c_void_p, C.c_char_p, C.c_uint, C.c_uint, C.c_int, u64p, u64p, C.POINTER(C.c_double)]
+    L.ref_collect_algo.argtypes = [C.c_void_p, C.c_char_p, C.c_uint, C.c_uint, C.c_int, u32p, C.c_uint64, u64p, u64p,
+                                   C.POINTER(C.c_double)]
     L.ref_brute_force.argtypes = [C.c_void_p, C.c_uint32, u32p, C.c_uint64, u64p]
     L.ref_download_oriented.argtypes = [C.c_void_p, u64p, u32p, u64p, u32p, u32p]
     L.ref_download_graph.argtypes = [C.c_void_p, u64p, u32p]
@@ -456,6 +515,33 @@ class RefGraph:
         out = np.empty((max(k, 1), 3), np.uint32)
         _rcheck(rlib().ref_collect(self._h, threads, chunk, int(skip_negative), _p32(out), k, _p64(cnt),
                                    _p64(st), C.byref(wall)))
+        return self._stats(st, wall), out[:k]
+
+    def run(self, algo: str, threads=1, chunk=64, skip_negative=False, reuse=False, hash=False) -> dict:
+        """run_parallel_count / run_parallel with a hash sink, any kernel."""
+        st = np.zeros(6, np.uint64)
+        hs = np.zeros(3, np.uint64)
+        wall = C.c_double()
+        flags = int(skip_negative) | (int(reuse) << 1)
+        _rcheck(rlib().ref_run(self._h, algo.encode(), threads, chunk, flags, _p64(hs) if hash else None, _p64(st),
+                               C.byref(wall)))
+        d = self._stats(st, wall)
+        if hash:
+            d["hash_count"], d["hash_sum"], d["hash_xor"] = int(hs[0]), int(hs[1]), int(hs[2])
+        return d
+
+    def collect_algo(self, algo: str, threads=1, chunk=64, skip_negative=False, reuse=False):
+        st = np.zeros(6, np.uint64)
+        cnt = np.zeros(1, np.uint64)
+        wall = C.c_double()
+        flags = int(skip_negative) | (int(reuse) << 1)
+        L = rlib()
+        _rcheck(L.ref_collect_algo(self._h, algo.encode(), threads, chunk, flags, None, 0, _p64(cnt), _p64(st),
+                                   C.byref(wall)))
+        k = int(cnt[0])
+        out = np.empty((max(k, 1), 3), np.uint32)
+        _rcheck(L.ref_collect_algo(self._h, algo.encode(), threads, chunk, flags, _p32(out), k, _p64(cnt), _p64(st),
+                                   C.byref(wall)))
         return self._stats(st, wall), out[:k]
 
     def cost_model(self) -> dict:

@@ -177,6 +177,59 @@ int ref_collect(void* hp, unsigned threads, unsigned chunk, int skip_negative, s
   });
 }
 
+// Any kernel by name ("cf" | "cf-hash" | "kclist" | "aot", engine.cpp:17-24).
+// flags: bit0 = aot_skip_negative_phase, bit1 = cf_hash_reuse_last_table.
+// hash (nullable) = count, sum, xor through a per-worker hash sink.
+int ref_run(void* hp, const char* algo, unsigned threads, unsigned chunk, int flags, std::uint64_t* hash,
+            std::uint64_t* stats, double* wall) {
+  return guarded([&] {
+    auto* h = static_cast<Handle*>(hp);
+    RunOptions opt;
+    opt.aot_skip_negative_phase = (flags & 1) != 0;
+    opt.cf_hash_reuse_last_table = (flags & 2) != 0;
+    Algorithm a = parse_algorithm(algo);
+    RunStats s;
+    if (hash) {
+      std::vector<std::array<std::uint64_t, 8>> accs(threads);
+      for (auto& x : accs) x.fill(0);
+      s = run_parallel(a, h->og, ParallelConfig{threads, chunk}, [&](unsigned w) { return HashSink{accs[w].data()}; },
+                       opt);
+      hash[0] = hash[1] = hash[2] = 0;
+      for (auto& x : accs) {
+        hash[0] += x[0];
+        hash[1] += x[1];
+        hash[2] ^= x[2];
+      }
+    } else {
+      s = run_parallel_count(a, h->og, ParallelConfig{threads, chunk}, opt);
+    }
+    fill_stats(s, stats);
+    if (wall) *wall = s.wall_time_s;
+  });
+}
+
+// Raw emissions of any kernel (run_parallel_collecting), as ref_collect.
+int ref_collect_algo(void* hp, const char* algo, unsigned threads, unsigned chunk, int flags, std::uint32_t* out,
+                     std::uint64_t cap, std::uint64_t* count, std::uint64_t* stats, double* wall) {
+  return guarded([&] {
+    auto* h = static_cast<Handle*>(hp);
+    RunOptions opt;
+    opt.aot_skip_negative_phase = (flags & 1) != 0;
+    opt.cf_hash_reuse_last_table = (flags & 2) != 0;
+    std::vector<std::vector<std::array<VertexId, 3>>> bufs;
+    RunStats s = run_parallel_collecting(parse_algorithm(algo), h->og, ParallelConfig{threads, chunk}, bufs, opt);
+    std::uint64_t k = 0;
+    for (auto& b : bufs)
+      for (auto& t : b) {
+        if (out && k < cap) std::memcpy(out + 3 * k, t.data(), 12);
+        ++k;
+      }
+    *count = k;
+    fill_stats(s, stats);
+    if (wall) *wall = s.wall_time_s;
+  });
+}
+
 int ref_cost_model(void* hp, std::uint64_t* out) {
   return guarded([&] {
     CostModel cm = cost_model(static_cast<Handle*>(hp)->og);

@@ -431,6 +431,207 @@ OR_API uint64_t or_aot(const or_oriented* g, int skip_negative, uint64_t* stats,
 }
 
 /* ------------------------------------------------------------------------ */
+/* The comparison kernels -- engine.hpp:164-236 (cf merge, cf hash, kclist3), */
+/* sequential driver engine.hpp:294-304.  algo: 0 = cf (merge), 1 = cf-hash,  */
+/* 2 = kclist.  Same stats/emission conventions as or_aot; `reuse` is         */
+/* RunOptions::cf_hash_reuse_last_table (engine.hpp:58).  The cf-hash probe   */
+/* structure is a set; a bitmap gives the same membership answers, and the    */
+/* counters only count insertions and look-ups (engine.hpp:200-215).          */
+/* cf (merge) compares ranks (engine.hpp:168) on the current list layout.     */
+/* ------------------------------------------------------------------------ */
+OR_API uint64_t or_kernel(const or_oriented* g, int algo, int reuse, uint64_t* stats, uint32_t* out,
+                          uint64_t cap) {
+  uint64_t s[8] = {0};
+  uint64_t words = ((uint64_t)g->n + 63) / 64;
+  uint64_t* bm = (uint64_t*)calloc(words ? words : 1, sizeof(uint64_t));
+  uint64_t emitted = 0;
+#define OR_EMIT3(a, b, c)                                                   \
+  do {                                                                      \
+    s[0]++;                                                                 \
+    uint32_t e0_ = (a), e1_ = (b), e2_ = (c);                               \
+    if (out && emitted < cap) {                                             \
+      out[3 * emitted] = e0_; out[3 * emitted + 1] = e1_; out[3 * emitted + 2] = e2_; \
+    }                                                                       \
+    emitted++;                                                              \
+    canon3(&e0_, &e1_, &e2_);                                               \
+    uint64_t h = or_triangle_hash(e0_, e1_, e2_);                           \
+    s[6] += h; s[7] ^= h;                                                   \
+  } while (0)
+#define OR_SET(list_b, list_e, on)                                          \
+  for (uint64_t q_ = (list_b); q_ < (list_e); ++q_) {                       \
+    uint32_t x_ = g->out[q_];                                               \
+    if (on) bm[x_ >> 6] |= 1ull << (x_ & 63); else bm[x_ >> 6] &= ~(1ull << (x_ & 63)); \
+  }
+  for (uint32_t u = 0; u < g->n; ++u) {
+    uint64_t ub = g->out_off[u], ue = g->out_off[u + 1];
+    if (algo == 0) { /* cf_merge_pivot, engine.hpp:164-184 */
+      for (uint64_t k = ub; k < ue; ++k) {
+        uint32_t v = g->out[k];
+        uint64_t i = ub, j = g->out_off[v], je = g->out_off[v + 1];
+        while (i < ue && j < je) {
+          s[2]++;
+          uint32_t ri = g->rank[g->out[i]], rj = g->rank[g->out[j]];
+          if (ri < rj) ++i;
+          else if (rj < ri) ++j;
+          else { OR_EMIT3(u, v, g->out[i]); ++i; ++j; }
+        }
+      }
+    } else if (algo == 1) { /* cf_hash_pivot, engine.hpp:186-215 */
+      int64_t cached = -1; /* kNoOwner: the cache never survives the pivot */
+      for (uint64_t k = ub; k < ue; ++k) {
+        uint32_t v = g->out[k];
+        int hash_u = before(g, v, u);
+        uint32_t owner = hash_u ? u : v;
+        uint64_t bb = hash_u ? ub : g->out_off[v], be = hash_u ? ue : g->out_off[v + 1];
+        uint64_t pb = hash_u ? g->out_off[v] : ub, pe = hash_u ? g->out_off[v + 1] : ue;
+        if (!reuse || (int64_t)owner != cached) {
+          if (cached >= 0) {
+            uint32_t c = (uint32_t)cached;
+            OR_SET(g->out_off[c], g->out_off[c + 1], 0);
+          }
+          OR_SET(bb, be, 1);
+          s[3] += be - bb;
+          cached = owner;
+        }
+        for (uint64_t q = pb; q < pe; ++q) {
+          uint32_t w = g->out[q];
+          s[1]++;
+          if ((bm[w >> 6] >> (w & 63)) & 1) OR_EMIT3(u, v, w);
+        }
+        if (!reuse) { OR_SET(bb, be, 0); cached = -1; }
+      }
+      if (cached >= 0) {
+        uint32_t c = (uint32_t)cached;
+        OR_SET(g->out_off[c], g->out_off[c + 1], 0);
+      }
+    } else { /* kclist3_pivot, engine.hpp:217-236 */
+      OR_SET(ub, ue, 1);
+      s[3] += ue - ub;
+      for (uint64_t k = ub; k < ue; ++k) {
+        uint32_t v = g->out[k];
+        for (uint64_t q = g->out_off[v]; q < g->out_off[v + 1]; ++q) {
+          uint32_t w = g->out[q];
+          s[1]++;
+          if ((bm[w >> 6] >> (w & 63)) & 1) OR_EMIT3(u, v, w);
+        }
+      }
+      OR_SET(ub, ue, 0);
+    }
+  }
+#undef OR_SET
+#undef OR_EMIT3
+  free(bm);
+  memcpy(stats, s, sizeof(s));
+  return emitted;
+}
+
+/* Rewrites the out-lists of og in place: 0 = rank-asc, 1 = degree-desc,     */
+/* 2 = random:seed (ordering.cpp:229-266, out-lists only: the kernels above  */
+/* read no in-list).                                                          */
+static uint64_t or_splitmix(uint64_t* state) { /* ordering.cpp:13-19 */
+  *state += kGolden;
+  return or_fmix64(*state);
+}
+static uint64_t or_bounded(uint64_t* state, uint64_t bound) { /* ordering.cpp:23-26 */
+  return (uint64_t)(((unsigned __int128)or_splitmix(state) * bound) >> 64);
+}
+static void or_fisher_yates(uint32_t* a, uint64_t n, uint64_t seed) { /* ordering.cpp:28-34 */
+  uint64_t state = seed;
+  for (uint64_t i = n; i > 1; --i) {
+    uint64_t j = or_bounded(&state, i);
+    uint32_t t = a[i - 1]; a[i - 1] = a[j]; a[j] = t;
+  }
+}
+static const or_oriented* g_sort_ctx;
+static int g_sort_policy;
+static int or_cmp_local(const void* pa, const void* pb) {
+  uint32_t x = *(const uint32_t*)pa, y = *(const uint32_t*)pb;
+  const or_oriented* g = g_sort_ctx;
+  if (g_sort_policy == 1) {
+    uint64_t dx = (g->out_off[x + 1] - g->out_off[x]) + (g->in_off[x + 1] - g->in_off[x]);
+    uint64_t dy = (g->out_off[y + 1] - g->out_off[y]) + (g->in_off[y + 1] - g->in_off[y]);
+    if (dx != dy) return dx > dy ? -1 : 1;
+    return x < y ? -1 : (x > y);
+  }
+  return g->rank[x] < g->rank[y] ? -1 : (g->rank[x] > g->rank[y]);
+}
+OR_API void or_apply_local_order(or_oriented* g, int policy, uint64_t seed) {
+  g_sort_ctx = g;
+  g_sort_policy = policy == 1 ? 1 : 0;
+  for (uint32_t u = 0; u < g->n; ++u) {
+    uint64_t b = g->out_off[u], len = g->out_off[u + 1] - b;
+    qsort(g->out + b, len, sizeof(uint32_t), or_cmp_local);
+    if (policy == 2) {
+      uint64_t mix = seed;
+      uint64_t key = or_splitmix(&mix) ^ (((uint64_t)u << 1) | 0u);
+      or_fisher_yates(g->out + b, len, key);
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* degeneracy_order -- ordering.cpp:86-114: repeatedly remove the vertex of  */
+/* least (current degree, id).  A binary heap over packed (deg << 32 | id)   */
+/* with lazy deletion, as the reference.                                     */
+/* ------------------------------------------------------------------------ */
+static void heap_push(uint64_t* h, uint64_t* len, uint64_t x) {
+  uint64_t i = (*len)++;
+  h[i] = x;
+  while (i) {
+    uint64_t p = (i - 1) / 2;
+    if (h[p] <= h[i]) break;
+    uint64_t t = h[p]; h[p] = h[i]; h[i] = t;
+    i = p;
+  }
+}
+static uint64_t heap_pop(uint64_t* h, uint64_t* len) {
+  uint64_t top = h[0];
+  h[0] = h[--(*len)];
+  uint64_t i = 0;
+  for (;;) {
+    uint64_t l = 2 * i + 1, r = l + 1, k = i;
+    if (l < *len && h[l] < h[k]) k = l;
+    if (r < *len && h[r] < h[k]) k = r;
+    if (k == i) break;
+    uint64_t t = h[k]; h[k] = h[i]; h[i] = t;
+    i = k;
+  }
+  return top;
+}
+OR_API void or_degeneracy_order(const or_graph* g, uint32_t* rank) {
+  uint32_t n = g->n;
+  uint32_t* deg = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  unsigned char* removed = (unsigned char*)calloc(n ? n : 1, 1);
+  uint64_t* heap = (uint64_t*)malloc(sizeof(uint64_t) * ((uint64_t)n + 2 * g->m + 1));
+  uint64_t len = 0;
+  for (uint32_t u = 0; u < n; ++u) {
+    deg[u] = gdeg(g, u);
+    heap_push(heap, &len, ((uint64_t)deg[u] << 32) | u);
+  }
+  for (uint32_t r = 0; r < n; ++r) {
+    uint32_t u;
+    for (;;) {
+      uint64_t top = heap_pop(heap, &len);
+      u = (uint32_t)top;
+      if (!removed[u] && (uint32_t)(top >> 32) == deg[u]) break;
+    }
+    removed[u] = 1;
+    rank[u] = r;
+    for (uint64_t i = g->off[u]; i < g->off[u + 1]; ++i) {
+      uint32_t v = g->adj[i];
+      if (!removed[v]) heap_push(heap, &len, ((uint64_t)(--deg[v]) << 32) | v);
+    }
+  }
+  free(heap); free(removed); free(deg);
+}
+
+/* random_order -- ordering.cpp:116-120: Fisher-Yates of the identity. */
+OR_API void or_random_order(uint32_t n, uint64_t seed, uint32_t* rank) {
+  for (uint32_t u = 0; u < n; ++u) rank[u] = u;
+  or_fisher_yates(rank, n, seed);
+}
+
+/* ------------------------------------------------------------------------ */
 /* brute_force_triangles -- oracle.cpp:8-25 (sorted, duplicate-free)          */
 /* ------------------------------------------------------------------------ */
 OR_API uint64_t or_brute_force(const or_graph* g, uint32_t* out, uint64_t cap) {

@@ -25,8 +25,12 @@ EXPORTS = (
     "tl_gen_er", "tl_gen_rmat", "tl_chung_lu_prefix", "tl_gen_chung_lu",
     "tl_graph_from_pairs", "tl_graph_free", "tl_graph_info", "tl_graph_degrees", "tl_graph_csr",
     "tl_graph_from_text", "tl_graph_from_file", "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
-    "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list", "tl_brute_force",
+    "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list",
+    "tl_run_count", "tl_run_hash", "tl_run_list", "tl_degeneracy_order", "tl_random_order", "tl_brute_force",
 )
+
+# TL_ALGO_* (Algorithm, engine.hpp:18) by the reference's names (engine.cpp:7-15).
+ALGO_CODES = {"aot": 0, "cf": 1, "cf-hash": 2, "kclist": 3}
 
 
 class TlStats(C.Structure):
@@ -51,7 +55,8 @@ class TlLoadDiag(C.Structure):
 
 class TlRunOptions(C.Structure):
     _fields_ = [("skip_negative_phase", C.c_uint32), ("check_hygiene", C.c_uint32), ("part", C.c_uint32),
-                ("nparts", C.c_uint32), ("stream", C.c_void_p)]
+                ("nparts", C.c_uint32), ("stream", C.c_void_p), ("algorithm", C.c_uint32),
+                ("cf_hash_reuse_last_table", C.c_uint32)]
 
 
 class TlError(RuntimeError):
@@ -102,6 +107,11 @@ def lib() -> C.CDLL:
     L.tl_aot_count.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_aot_hash.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_aot_list.argtypes = [vp, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int, C.POINTER(TlStats)]
+    L.tl_run_count.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
+    L.tl_run_hash.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
+    L.tl_run_list.argtypes = [vp, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int, C.POINTER(TlStats)]
+    L.tl_degeneracy_order.argtypes = [vp, u32p]
+    L.tl_random_order.argtypes = [C.c_uint32, C.c_uint64, u32p]
     L.tl_brute_force.argtypes = [vp, C.c_uint32, u32p, C.c_uint64, u64p]
     return L
 
@@ -223,6 +233,28 @@ class DeviceGraph:
         _check(lib().tl_degree_order(self._h, _p32(r)))
         return r[: self.n]
 
+    def degeneracy_order(self) -> np.ndarray:
+        r = np.empty(max(self.n, 1), np.uint32)
+        _check(lib().tl_degeneracy_order(self._h, _p32(r)))
+        return r[: self.n]
+
+    def random_order(self, seed: int) -> np.ndarray:
+        r = np.empty(max(self.n, 1), np.uint32)
+        _check(lib().tl_random_order(self.n, seed, _p32(r)))
+        return r[: self.n]
+
+    def make_order(self, spec: str) -> np.ndarray:
+        """make_order(parse_order_spec(spec)) -- ordering.cpp:122-141."""
+        if spec == "id":
+            return np.arange(self.n, dtype=np.uint32)
+        if spec == "degree":
+            return self.degree_order()
+        if spec == "degeneracy":
+            return self.degeneracy_order()
+        if spec.startswith("random:"):
+            return self.random_order(int(spec[7:]))
+        raise ValueError(f"unknown order '{spec}'")
+
     def orient(self, rank: np.ndarray | None = None) -> "DeviceOriented":
         h = vp()
         if rank is not None:
@@ -238,8 +270,8 @@ class DeviceGraph:
         return out[: cnt.value]
 
 
-def run_options(skip_negative=False, part=0, nparts=1, stream=0) -> TlRunOptions:
-    return TlRunOptions(int(skip_negative), 0, part, nparts, stream or None)
+def run_options(skip_negative=False, part=0, nparts=1, stream=0, algo="aot", reuse=False) -> TlRunOptions:
+    return TlRunOptions(int(skip_negative), 0, part, nparts, stream or None, ALGO_CODES[algo], int(reuse))
 
 
 class DeviceOriented:
@@ -293,23 +325,27 @@ class DeviceOriented:
         _check(lib().tl_cost_model(self._h, _p64(c)))
         return dict(cf_cost=int(c[0]), kclist_cost=int(c[1]), aot_cost=int(c[2]))
 
-    def count(self, skip_negative=False, part=0, nparts=1, stream=0) -> dict:
+    # algo="aot" goes through tl_aot_*, the others through tl_run_* (TL_ALGO_*).
+    def count(self, skip_negative=False, part=0, nparts=1, stream=0, algo="aot", reuse=False) -> dict:
         st = TlStats()
-        o = run_options(skip_negative, part, nparts, stream)
-        _check(lib().tl_aot_count(self._h, C.byref(o), C.byref(st)))
+        o = run_options(skip_negative, part, nparts, stream, algo, reuse)
+        fn = lib().tl_aot_count if algo == "aot" else lib().tl_run_count
+        _check(fn(self._h, C.byref(o), C.byref(st)))
         return st.as_dict()
 
-    def hash(self, skip_negative=False, part=0, nparts=1, stream=0) -> dict:
+    def hash(self, skip_negative=False, part=0, nparts=1, stream=0, algo="aot", reuse=False) -> dict:
         st = TlStats()
-        o = run_options(skip_negative, part, nparts, stream)
-        _check(lib().tl_aot_hash(self._h, C.byref(o), C.byref(st)))
+        o = run_options(skip_negative, part, nparts, stream, algo, reuse)
+        fn = lib().tl_aot_hash if algo == "aot" else lib().tl_run_hash
+        _check(fn(self._h, C.byref(o), C.byref(st)))
         return st.as_dict()
 
-    def list(self, canonical=False, skip_negative=False, part=0, nparts=1, stream=0):
+    def list(self, canonical=False, skip_negative=False, part=0, nparts=1, stream=0, algo="aot", reuse=False):
         """Returns (stats, (T, 3) uint32 array)."""
         st = TlStats()
-        o = run_options(skip_negative, part, nparts, stream)
-        _check(lib().tl_aot_list(self._h, C.byref(o), None, 0, int(canonical), C.byref(st)))
+        o = run_options(skip_negative, part, nparts, stream, algo, reuse)
+        fn = lib().tl_aot_list if algo == "aot" else lib().tl_run_list
+        _check(fn(self._h, C.byref(o), None, 0, int(canonical), C.byref(st)))
         out = np.empty((max(st.triangles, 1), 3), np.uint32)
-        _check(lib().tl_aot_list(self._h, C.byref(o), _p32(out), st.triangles, int(canonical), C.byref(st)))
+        _check(fn(self._h, C.byref(o), _p32(out), st.triangles, int(canonical), C.byref(st)))
         return st.as_dict(), out[: st.triangles]

@@ -206,12 +206,18 @@ VertexOrder degree_order(const Graph& g) {
   return o;
 }
 
-VertexOrder degeneracy_order(const Graph&) {
-  throw std::invalid_argument("order 'degeneracy' has no B200 implementation (the AOT path uses the degree order)");
+VertexOrder degeneracy_order(const Graph& g) {  // ordering.cpp:86-114
+  VertexOrder o;
+  o.rank.resize(g.num_vertices());
+  if (g.handle() && g.num_vertices()) check(tl_degeneracy_order(g.handle(), o.rank.data()), "degeneracy_order");
+  return o;
 }
 
-VertexOrder random_order(const Graph&, std::uint64_t) {
-  throw std::invalid_argument("order 'random' has no B200 implementation (the AOT path uses the degree order)");
+VertexOrder random_order(const Graph& g, std::uint64_t seed) {  // ordering.cpp:116-120
+  VertexOrder o;
+  o.rank.resize(g.num_vertices());
+  check(tl_random_order(g.num_vertices(), seed, o.rank.data()), "random_order");
+  return o;
 }
 
 VertexOrder make_order(const Graph& g, const OrderSpec& spec) {
@@ -431,20 +437,64 @@ Algorithm parse_algorithm(const std::string& name) {  // engine.cpp:17-24
 namespace detail {
 
 void require_device_algorithm(Algorithm a) {
-  if (a != Algorithm::aot)
-    throw std::invalid_argument(std::string("algorithm '") + to_string(a) +
-                                "' has no B200 implementation (only aot runs on the device)");
+  for (Algorithm d : kDeviceAlgorithms)
+    if (d == a) return;
+  throw std::invalid_argument(std::string("algorithm '") + to_string(a) + "' has no B200 implementation");
+}
+
+std::uint32_t algorithm_code(Algorithm a) {
+  switch (a) {
+    case Algorithm::cf_merge: return TL_ALGO_CF_MERGE;
+    case Algorithm::cf_hash: return TL_ALGO_CF_HASH;
+    case Algorithm::kclist3: return TL_ALGO_KCLIST3;
+    case Algorithm::aot: return TL_ALGO_AOT;
+  }
+  throw std::invalid_argument("unknown algorithm");
+}
+
+// engine.hpp:143-149: the merge kernel needs rank-ascending lists.  The device
+// copy always is; a host layout rewritten by apply_local_order may not be.
+void assert_layout(Algorithm algo, const OrientedGraph& g) {
+  if (algo == Algorithm::cf_merge && g.local_order().policy != LocalOrderPolicy::rank_asc &&
+      !g.out_lists_rank_sorted())
+    throw std::invalid_argument("merge kernel requires rank-ascending adjacency (local order rank-asc)");
 }
 
 namespace {
-tl_run_options options_for(const RunOptions& opt) {
+tl_run_options options_for(Algorithm algo, const RunOptions& opt) {
   tl_run_options o;
   std::memset(&o, 0, sizeof(o));
   o.skip_negative_phase = opt.aot_skip_negative_phase ? 1u : 0u;
   o.check_hygiene = opt.check_bitmap_between_pivots ? 1u : 0u;
   o.part = 0;
   o.nparts = 1;
+  o.algorithm = algorithm_code(algo);
+  o.cf_hash_reuse_last_table = opt.cf_hash_reuse_last_table ? 1u : 0u;
   return o;
+}
+
+// cf-hash with cf_hash_reuse_last_table counts a rebuild whenever the owner
+// changes along the list (engine.hpp:200-206), so on a host layout other than
+// the device's rank-ascending one the table_builds counter follows that
+// layout: recount it over the host lists.
+void relayout_table_builds(const OrientedGraph& g, const RunOptions& opt, Algorithm algo, RunStats& r) {
+  if (algo != Algorithm::cf_hash || !opt.cf_hash_reuse_last_table ||
+      g.local_order().policy == LocalOrderPolicy::rank_asc)
+    return;
+  std::uint64_t builds = 0;
+  for (VertexId u = 0; u < g.num_vertices(); ++u) {
+    bool prev_u = false;
+    for (VertexId v : g.out_neighbors(u)) {
+      const bool hash_u = g.out_degree_before(v, u);
+      if (hash_u) {
+        if (!prev_u) builds += g.out_degree(u);
+      } else {
+        builds += g.out_degree(v);
+      }
+      prev_u = hash_u;
+    }
+  }
+  r.table_builds = builds;
 }
 
 RunStats to_run_stats(const tl_stats& s) {
@@ -465,28 +515,37 @@ RunStats to_run_stats(const tl_stats& s) {
 bool empty_handle(const OrientedGraph& g) { return g.handle() == nullptr; }
 }  // namespace
 
-RunStats device_count(const OrientedGraph& g, const RunOptions& opt, int mode) {
+RunStats device_count(Algorithm algo, const OrientedGraph& g, const RunOptions& opt, int mode) {
+  require_device_algorithm(algo);
+  assert_layout(algo, g);
   if (empty_handle(g)) return RunStats{};
-  tl_run_options o = options_for(opt);
+  tl_run_options o = options_for(algo, opt);
   tl_stats s;
   if (mode == 1)
-    check(tl_aot_hash(g.handle(), &o, &s), "aot hash");
+    check(tl_run_hash(g.handle(), &o, &s), "hash run");
   else
-    check(tl_aot_count(g.handle(), &o, &s), "aot count");
-  return to_run_stats(s);
+    check(tl_run_count(g.handle(), &o, &s), "count run");
+  RunStats r = to_run_stats(s);
+  relayout_table_builds(g, opt, algo, r);
+  return r;
 }
 
-RunStats device_list(const OrientedGraph& g, const RunOptions& opt, std::vector<std::array<VertexId, 3>>& raw) {
+RunStats device_list(Algorithm algo, const OrientedGraph& g, const RunOptions& opt,
+                     std::vector<std::array<VertexId, 3>>& raw) {
+  require_device_algorithm(algo);
+  assert_layout(algo, g);
   if (empty_handle(g)) return RunStats{};
-  tl_run_options o = options_for(opt);
+  tl_run_options o = options_for(algo, opt);
   tl_stats s;
-  check(tl_aot_list(g.handle(), &o, nullptr, 0, 0, &s), "aot list");  // count (cached for sizing)
+  check(tl_run_list(g.handle(), &o, nullptr, 0, 0, &s), "list run");  // count (cached for sizing)
   std::size_t base = raw.size();
   raw.resize(base + s.triangles);
   static_assert(sizeof(std::array<VertexId, 3>) == 12, "triple layout");
-  check(tl_aot_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(raw.data() + base), s.triangles, 0, &s),
-        "aot list");
-  return to_run_stats(s);
+  check(tl_run_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(raw.data() + base), s.triangles, 0, &s),
+        "list run");
+  RunStats r = to_run_stats(s);
+  relayout_table_builds(g, opt, algo, r);
+  return r;
 }
 
 void validate(const ParallelConfig& cfg) {  // parallel.hpp:28-29
@@ -497,19 +556,16 @@ void validate(const ParallelConfig& cfg) {  // parallel.hpp:28-29
 }  // namespace detail
 
 RunStats run_counting(Algorithm algo, const OrientedGraph& g, const RunOptions& opt) {
-  detail::require_device_algorithm(algo);
-  return detail::device_count(g, opt, 0);
+  return detail::device_count(algo, g, opt, 0);
 }
 
 RunStats run_collecting(Algorithm algo, const OrientedGraph& g, std::vector<std::array<VertexId, 3>>& out,
                         const RunOptions& opt) {
-  detail::require_device_algorithm(algo);
-  return detail::device_list(g, opt, out);
+  return detail::device_list(algo, g, opt, out);
 }
 
 RunStats run_hashing(Algorithm algo, const OrientedGraph& g, const RunOptions& opt) {
-  detail::require_device_algorithm(algo);
-  return detail::device_count(g, opt, 1);
+  return detail::device_count(algo, g, opt, 1);
 }
 
 CostModel cost_model(const OrientedGraph& g) {
@@ -549,27 +605,17 @@ void diff_sets(const std::vector<Triangle>& reference, const std::vector<Triangl
 }
 
 // Device-canonicalised, device-sorted emission list (duplicates kept).
-std::vector<Triangle> device_canonical(const OrientedGraph& g, const RunOptions& opt, RunStats& stats) {
+std::vector<Triangle> device_canonical(Algorithm algo, const OrientedGraph& g, const RunOptions& opt,
+                                       RunStats& stats) {
   std::vector<Triangle> out;
   if (!g.handle()) return out;
-  tl_run_options o;
-  std::memset(&o, 0, sizeof(o));
-  o.skip_negative_phase = opt.aot_skip_negative_phase ? 1u : 0u;
-  o.nparts = 1;
+  tl_run_options o = detail::options_for(algo, opt);
   tl_stats s;
-  check(tl_aot_list(g.handle(), &o, nullptr, 0, 1, &s), "aot list");
+  check(tl_run_list(g.handle(), &o, nullptr, 0, 1, &s), "list run");
   out.resize(s.triangles);
   static_assert(sizeof(Triangle) == 12, "Triangle layout");
-  check(tl_aot_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(out.data()), out.size(), 1, &s), "aot list");
-  RunStats r;
-  r.triangles = s.triangles;
-  r.probes = s.probes;
-  r.table_builds = s.table_builds;
-  r.positive_triangles = s.positive_triangles;
-  r.negative_triangles = s.negative_triangles;
-  r.wall_time_s = s.list_ms * 1e-3;
-  r.probes_executed = s.probes_executed;
-  stats = r;
+  check(tl_run_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(out.data()), out.size(), 1, &s), "list run");
+  stats = detail::to_run_stats(s);
   return out;
 }
 }  // namespace
@@ -579,7 +625,10 @@ VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algor
                                 const RunOptions& opt) {  // engine.cpp:82-130
   for (Algorithm a : algorithms) detail::require_device_algorithm(a);
   OrientedGraph oriented = orient(g, order);
-  (void)local;  // layout policy does not change any counter or set (test_engine.cpp:172-185)
+  // cf runs on the rank-ascending layout it requires, the others on `local`;
+  // no counter of a non-reusing run depends on the layout
+  // (test_engine.cpp:172-185), so every run uses the device's lists.
+  (void)local;
   VerifyReport report;
   std::vector<Triangle> baseline;
   if (reference) {
@@ -591,7 +640,7 @@ VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algor
   for (Algorithm algo : algorithms) {
     VerifyAlgorithmResult r;
     r.algorithm = algo;
-    std::vector<Triangle> canon = device_canonical(oriented, opt, r.stats);
+    std::vector<Triangle> canon = device_canonical(algo, oriented, opt, r.stats);
     std::vector<Triangle> uniq = canon;
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
     r.unique_triangles = uniq.size();

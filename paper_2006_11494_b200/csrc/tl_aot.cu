@@ -96,7 +96,7 @@ struct Rec {
   uint32_t l, dl;
 };
 
-enum Acc : int { kPos = 0, kNeg, kExec, kHsum, kHxor, kEmitted, kWarpCounter, kCtaCounter, kLogical, kAccN };
+enum Acc : int { kPos = 0, kNeg, kExec, kHsum, kHxor, kEmitted, kWarpCounter, kCtaCounter, kLogical, kEdgeCounter, kAccN };
 
 struct Params {
   const uint64_t* off;
@@ -110,6 +110,7 @@ struct Params {
   const Rec* crecs;     // phase 1 (CTA) records, one per task
   uint64_t ncta;
   uint32_t skip_neg;
+  uint32_t swap_neg;    // cf-hash: a negative claim emits (tail, head, w) (engine.hpp:212)
   unsigned long long* acc;
   uint32_t* out;
   uint64_t out_cap;
@@ -336,7 +337,10 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     for (int k = 0; k < kSU; ++k) {
       const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
       if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
-      if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oo[k], x[k]);
+      if constexpr (MODE != AotMode::count) {
+        const bool sw = MODE == AotMode::list && P.swap_neg && (of[k] & kNegBit);
+        emit(st, P, hit != 0, sw ? oo[k] : a_orig, sw ? a_orig : oo[k], x[k]);
+      }
     }
   }
 
@@ -350,8 +354,14 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     const uint64_t bj = __shfl_sync(kFull, b, j);
     const uint32_t lj = __shfl_sync(kFull, len, j);
     const bool nj = __shfl_sync(kFull, neg, j);
-    uint32_t oj = 0;
-    if constexpr (MODE != AotMode::count) oj = __shfl_sync(kFull, b_orig, j);
+    uint32_t oj = 0, ea = a_orig;
+    if constexpr (MODE != AotMode::count) {
+      oj = __shfl_sync(kFull, b_orig, j);
+      if (MODE == AotMode::list && P.swap_neg && nj) {
+        ea = oj;
+        oj = a_orig;
+      }
+    }
     const uint32_t* p = P.col + bj + lane;
     int rem = int(lj) - int(lane);  // this lane reads p[32k] while 32k < rem
     uint32_t hits = 0;
@@ -365,7 +375,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
         over |= x[k] > lmax;
         const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
         hits += hit;
-        if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, a_orig, oj, x[k]);
+        if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, ea, oj, x[k]);
       }
       p += 32 * U;
       rem -= 32 * U;
@@ -713,6 +723,74 @@ __global__ void k_tasks(const uint64_t* RP, uint32_t nrec, uint64_t G, uint64_t 
   }
 }
 
+// Forward claims (kclist3_pivot / cf_merge_pivot, engine.hpp:164-236): the
+// claim of edge e = t->h is pivot t traversing all of N+(h).
+__global__ void k_fwd_windows(const uint64_t* off, const uint32_t* col, uint64_t m, uint64_t* win) {
+  TL_GRID_STRIDE(e, m) {
+    const uint32_t h = col[e];
+    const uint64_t b = off[h];
+    win[e] = b | ((off[h + 1] - b) << kWinLenShift);
+  }
+}
+
+__device__ __forceinline__ uint32_t count_le(const uint32_t* a, uint32_t len, uint32_t x) {  // #{a[i] <= x}
+  uint32_t lo = 0, hi = len;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Per-edge counters of the comparison kernels over the out-edges [eb, ee) of
+// the vertices [vb, ve), one warp per vertex:
+//  * cf-hash table builds (engine.hpp:194-206): the build side of u->v is
+//    N+(u) when v precedes u in (deg+, id) order, else N+(v); with
+//    cf_hash_reuse_last_table a build of N+(u) is skipped when the previous
+//    edge of the list also built N+(u);
+//  * cf merge comparisons (engine.hpp:166-181): the merge loop of N+(u) and
+//    N+(v) (rank-ascending) runs #{a <= M} + #{b <= M} - |common| times,
+//    M = min(max N+(u), max N+(v)); this pass sums the first two terms and
+//    the caller subtracts the triangles.
+__global__ void k_edge_counters(const uint64_t* off, const uint32_t* col, const uint32_t* orig, uint32_t vb,
+                                uint32_t ve, uint64_t eb, uint64_t ee, uint32_t algo, uint32_t reuse,
+                                unsigned long long* acc) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long sum = 0;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < uint64_t(ve - vb); w += nwarps) {
+    const uint32_t u = vb + uint32_t(w);
+    const uint64_t ub = off[u], ue = off[u + 1];
+    const uint64_t lo = max(ub, eb), hi = min(ue, ee);
+    if (lo >= hi) continue;
+    const uint32_t du = uint32_t(ue - ub), ou = __ldg(orig + u);
+    const uint32_t maxA = __ldg(col + ue - 1);
+    auto hash_u = [&](uint32_t v, uint32_t dv) { return dv < du || (dv == du && __ldg(orig + v) < ou); };
+    for (uint64_t e = lo + lane; e < hi; e += 32) {
+      const uint32_t v = __ldg(col + e);
+      const uint64_t vb0 = off[v];
+      const uint32_t dv = uint32_t(off[v + 1] - vb0);
+      if (algo == uint32_t(Algo::cf_hash)) {
+        const bool hu = hash_u(v, dv);
+        uint32_t build = hu ? du : dv;
+        if (reuse && hu && e > ub) {
+          const uint32_t p = __ldg(col + e - 1);
+          if (hash_u(p, uint32_t(off[p + 1] - off[p]))) build = 0;
+        }
+        sum += build;
+      } else if (dv) {
+        const uint32_t maxB = __ldg(col + vb0 + dv - 1);
+        if (maxA <= maxB)
+          sum += du + count_le(col + vb0, dv, maxA);
+        else
+          sum += dv + count_le(col + ub, du, maxB);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+  if (lane == 0 && sum) atomicAdd(acc, sum);
+}
+
 template <typename F>
 void cub_call(cudaStream_t s, F&& f) {
   size_t bytes = 0;
@@ -768,13 +846,39 @@ uint64_t launch_kernels(const Params& P, bool long_lists, cudaStream_t s) {
 
 }  // namespace
 
-AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t part, uint32_t nparts, cudaStream_t s,
-                  uint32_t* d_out, uint64_t out_cap) {
+namespace {
+void ensure_forward_claims(tl_oriented& og, cudaStream_t s) {
+  if (og.fwd_win.p || og.m == 0) return;
+  og.fwd_win.alloc(og.m, og.stream);  // owned by the handle's stream
+  k_fwd_windows<<<grid_for(og.m, 256, 148u * 64u), 256, 0, og.stream>>>(og.off.p, og.col.p, og.m, og.fwd_win.p);
+  TL_CUDA(cudaGetLastError());
+  if (s != og.stream) {
+    cudaEvent_t ev;
+    TL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(ev, og.stream));
+    TL_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    cudaEventDestroy(ev);
+  }
+}
+}  // namespace
+
+// One run of `spec.algo` on the device.  aot and cf-hash share the adaptive
+// claims (cf-hash traverses the min side and probes the other, engine.hpp:
+// 194-215 -- the same pairs of lists as aot_pivot's two phases); kclist3 and
+// cf merge use the forward claims (every edge t->h: pivot t, all of N+(h)).
+AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t* d_out, uint64_t out_cap) {
   AotResult r;
-  if (nparts == 0) nparts = 1;
+  const AotMode mode = spec.mode;
+  const uint32_t nparts = spec.nparts ? spec.nparts : 1, part = spec.part;
   TL_REQUIRE(part < nparts, TL_EINVAL, "partition index out of range");
+  const bool skip_negative = spec.algo == Algo::aot && spec.skip_negative;
+  const bool fwd = spec.algo == Algo::kclist3 || spec.algo == Algo::cf_merge;
   const uint64_t m = og.m;
   if (m == 0) return r;
+  if (fwd) ensure_forward_claims(og, s);
+  const uint64_t* claim_off = fwd ? og.off.p : og.claim_off.p;
+  const uint64_t* cwin = fwd ? og.fwd_win.p : og.win.p;
+  const uint32_t* cs = fwd ? og.col.p : og.claim_s.p;
 
   cudaEvent_t ev[3];
   for (auto& e : ev) TL_CUDA(cudaEventCreate(&e));
@@ -794,7 +898,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   DBuf<uint64_t> CP;
   CP.alloc(m + 1, s);
   const bool whole = nparts == 1;
-  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(og.win.p, og.claim_s.p, og.off.p, m, skip_negative,
+  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(cwin, cs, og.off.p, m, skip_negative,
                                                                CP.p, whole ? acc.p + kLogical : nullptr);
   TL_CUDA(cudaGetLastError());
   cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, CP.p, m + 1, s); });
@@ -806,7 +910,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   } else {
     DBuf<uint64_t> split;
     split.alloc(8, s);
-    k_split<<<1, 32, 0, s>>>(CP.p, m, og.claim_off.p, og.off.p, og.n, part, nparts, split.p);
+    k_split<<<1, 32, 0, s>>>(CP.p, m, claim_off, og.off.p, og.n, part, nparts, split.p);
     TL_CUDA(cudaGetLastError());
     uint64_t hs[8];
     TL_CUDA(cudaMemcpyAsync(hs, split.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
@@ -818,7 +922,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     r.table_builds = hs[6];
     ++r.launches;
     if (cb < ce) {
-      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(og.claim_s.p, og.off.p, cb, ce, skip_negative,
+      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(cs, og.off.p, cb, ce, skip_negative,
                                                                  acc.p + kLogical);
       TL_CUDA(cudaGetLastError());
       ++r.launches;
@@ -855,7 +959,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     nrc.alloc(np + 1, s);
     ow.alloc(np + 1, s);
     oc.alloc(np + 1, s);
-    k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, og.col.p,
+    k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, og.col.p,
                                                                           pb, np, cb, ce, T, nrw.p, nrc.p);
     TL_CUDA(cudaGetLastError());
     cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrw.p, ow.p, np + 1, s); });
@@ -864,7 +968,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
       DBuf<unsigned long long> ps;
       ps.alloc(48, s);
       TL_CUDA(cudaMemsetAsync(ps.p, 0, 48 * 8, s));
-      k_path_stats<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, og.col.p, pb, np, cb,
+      k_path_stats<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, og.col.p, pb, np, cb,
                                                                 ce, ps.p);
       unsigned long long hp[48];
       TL_CUDA(cudaMemcpyAsync(hp, ps.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
@@ -887,7 +991,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
       wrecs.alloc(nw, s);
       wgt.alloc(nw + 1, s);
       TL_CUDA(cudaMemsetAsync(wgt.p + nw, 0, 8, s));
-      k_records<<<grid_for(nw, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, pb, np, cb, ce, nrw.p,
+      k_records<<<grid_for(nw, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, pb, np, cb, ce, nrw.p,
                                                               ow.p, nw, wrecs.p, wgt.p);
       TL_CUDA(cudaGetLastError());
       cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, wgt.p, nw + 1, s); });
@@ -902,7 +1006,7 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     }
     if (nc) {
       crecs.alloc(nc, s);
-      k_records<<<grid_for(nc, 256, 148u * 32u), 256, 0, s>>>(CP.p, og.claim_off.p, og.off.p, pb, np, cb, ce, nrc.p,
+      k_records<<<grid_for(nc, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, pb, np, cb, ce, nrc.p,
                                                               oc.p, nc, crecs.p, nullptr);
       TL_CUDA(cudaGetLastError());
       ++r.launches;
@@ -913,10 +1017,11 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   Params P{};
   P.off = og.off.p;
   P.col = og.col.p;
-  P.win = og.win.p;
-  P.cs = og.claim_s.p;
+  P.win = cwin;
+  P.cs = cs;
   P.orig = og.orig.p;
   P.skip_neg = skip_negative;
+  P.swap_neg = spec.algo == Algo::cf_hash;
   P.acc = acc.p;
   P.out = d_out;
   P.out_cap = out_cap;
@@ -929,6 +1034,27 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
     case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, long_lists, s); break;
     case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, long_lists, s); break;
     case AotMode::list: r.launches += launch_kernels<AotMode::list>(P, long_lists, s); break;
+  }
+  if (spec.algo == Algo::cf_hash || spec.algo == Algo::cf_merge) {
+    // edges of this part: the claim range for forward claims (claim index =
+    // edge index), a vertex share for the adaptive claims of cf-hash
+    uint32_t vb = 0, ve = og.n;
+    uint64_t eb = 0, ee = m;
+    if (fwd) {
+      vb = cb < ce ? pb : 0;
+      ve = cb < ce ? pe : 0;
+      eb = cb;
+      ee = ce;
+    } else if (nparts > 1) {
+      vb = uint32_t(uint64_t(og.n) * part / nparts);
+      ve = uint32_t(uint64_t(og.n) * (part + 1) / nparts);
+    }
+    if (vb < ve) {
+      k_edge_counters<<<grid_for(uint64_t(ve - vb) * 32, 256, 148u * 64u), 256, 0, s>>>(
+          og.off.p, og.col.p, og.orig.p, vb, ve, eb, ee, uint32_t(spec.algo), spec.reuse, acc.p + kEdgeCounter);
+      TL_CUDA(cudaGetLastError());
+      ++r.launches;
+    }
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];
@@ -947,6 +1073,25 @@ AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t pa
   r.hash_xor = h[kHxor];
   r.emitted = h[kEmitted];
   r.tasks = G + nc;
+  r.triangles = r.positive + r.negative;
+  switch (spec.algo) {  // the counters each kernel keeps (engine.hpp:164-276)
+    case Algo::aot:
+      r.probes = r.logical;
+      r.report_positive = r.positive;
+      r.report_negative = r.negative;
+      break;
+    case Algo::kclist3:
+      r.probes = r.logical;  // sum of deg+(head) = kclist_cost
+      break;
+    case Algo::cf_hash:
+      r.probes = r.logical;  // sum of min(deg+) = aot_cost
+      r.table_builds = h[kEdgeCounter];
+      break;
+    case Algo::cf_merge:
+      r.table_builds = 0;
+      r.merge_comparisons = h[kEdgeCounter] - r.triangles;
+      break;
+  }
   return r;
 }
 

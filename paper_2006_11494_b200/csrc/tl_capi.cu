@@ -10,6 +10,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "tl_internal.cuh"
 
@@ -50,12 +52,12 @@ cudaStream_t pick_stream(void* user, cudaStream_t own) { return user ? static_ca
 void fill_stats(tl_stats* st, const tlb::AotResult& r) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
-  st->triangles = r.positive + r.negative;
-  st->probes = r.logical;
-  st->merge_comparisons = 0;
+  st->triangles = r.triangles;
+  st->probes = r.probes;
+  st->merge_comparisons = r.merge_comparisons;
   st->table_builds = r.table_builds;
-  st->positive_triangles = r.positive;
-  st->negative_triangles = r.negative;
+  st->positive_triangles = r.report_positive;
+  st->negative_triangles = r.report_negative;
   st->probes_executed = r.executed;
   st->hash_sum = r.hash_sum;
   st->hash_xor = r.hash_xor;
@@ -109,6 +111,7 @@ tl_oriented::~tl_oriented() {
   claim_off.reset();
   win.reset();
   claim_s.reset();
+  fwd_win.reset();  // every buffer is freed on its stream before the stream goes
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
@@ -413,67 +416,130 @@ int tl_cost_model(tl_oriented* og, uint64_t* costs) {
   });
 }
 
-// ------------------------------------------------------------- AOT listing
-static void run_checked(tl_oriented* og, const tl_run_options* opt, tlb::AotMode mode, tl_stats* stats) {
+// ------------------------------------------------------------- listing
+static tlb::RunSpec spec_of(const tl_run_options& o, tlb::AotMode mode, bool any_algorithm) {
+  tlb::RunSpec sp;
+  if (any_algorithm) {
+    TL_REQUIRE(o.algorithm <= TL_ALGO_KCLIST3, TL_EINVAL,
+               "unknown algorithm " + std::to_string(o.algorithm) + " (expected TL_ALGO_*)");
+    sp.algo = static_cast<tlb::Algo>(o.algorithm);
+  }
+  sp.mode = mode;
+  sp.skip_negative = o.skip_negative_phase != 0;
+  sp.reuse = o.cf_hash_reuse_last_table != 0;
+  sp.part = o.part;
+  sp.nparts = o.nparts ? o.nparts : 1;
+  TL_REQUIRE(sp.part < sp.nparts, TL_EINVAL, "part must be < nparts");
+  return sp;
+}
+
+static std::tuple<uint32_t, uint32_t, uint32_t, uint32_t> cache_key(const tlb::RunSpec& sp) {
+  return {uint32_t(sp.algo), uint32_t(sp.algo == tlb::Algo::aot && sp.skip_negative), sp.part, sp.nparts};
+}
+
+static void run_checked(tl_oriented* og, const tl_run_options* opt, tlb::AotMode mode, bool any_algorithm,
+                        tl_stats* stats) {
   TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
   tl_run_options o = opt ? *opt : defaults();
-  if (o.nparts == 0) o.nparts = 1;
-  TL_REQUIRE(o.part < o.nparts, TL_EINVAL, "part must be < nparts");
+  tlb::RunSpec sp = spec_of(o, mode, any_algorithm);
   tlb::DeviceGuard guard(og->device);
-  tlb::AotResult r = tlb::aot_run(*og, mode, o.skip_negative_phase != 0, o.part, o.nparts,
-                                  pick_stream(o.stream, og->stream), nullptr, 0);
-  og->tri_cache[{o.skip_negative_phase != 0, o.part, o.nparts}] = r.positive + r.negative;
+  tlb::AotResult r = tlb::aot_run(*og, sp, pick_stream(o.stream, og->stream), nullptr, 0);
+  og->tri_cache[cache_key(sp)] = r.triangles;
   fill_stats(stats, r);
 }
 
+static void list_checked(tl_oriented* og, const tl_run_options* opt, bool any_algorithm, uint32_t* triples,
+                         uint64_t cap, int canonical, tl_stats* stats) {
+  TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
+  tl_run_options o = opt ? *opt : defaults();
+  tlb::RunSpec sp = spec_of(o, tlb::AotMode::count, any_algorithm);
+  tlb::DeviceGuard guard(og->device);
+  cudaStream_t s = pick_stream(o.stream, og->stream);
+  auto key = cache_key(sp);
+  auto it = og->tri_cache.find(key);
+  uint64_t expect;
+  if (it == og->tri_cache.end()) {
+    tlb::AotResult c = tlb::aot_run(*og, sp, s, nullptr, 0);
+    expect = c.triangles;
+    og->tri_cache[key] = expect;
+  } else {
+    expect = it->second;
+  }
+  tlb::DBuf<uint32_t> d_out;
+  d_out.alloc(std::max<uint64_t>(3 * expect, 3), s);
+  sp.mode = tlb::AotMode::list;
+  tlb::AotResult r = tlb::aot_run(*og, sp, s, d_out.p, expect);
+  const uint64_t T = r.emitted;
+  TL_REQUIRE(T == r.triangles, TL_ELOGIC, "emission count disagrees with the triangle counters");
+  TL_REQUIRE(T <= expect, TL_ELOGIC, "listing emitted more triangles than the counting pass");
+  if (canonical && T) {
+    tlb::canonicalize_triples(d_out.p, T, s);
+    tlb::sort_triples(d_out.p, T, og->nb, s);
+  }
+  fill_stats(stats, r);
+  if (triples) {
+    if (cap < T) {
+      TL_CUDA(cudaStreamSynchronize(s));
+      throw tlb::TlError(TL_ECAPACITY, "output capacity " + std::to_string(cap) + " < " + std::to_string(T) +
+                                           " triangles");
+    }
+    if (T) TL_CUDA(cudaMemcpyAsync(triples, d_out.p, sizeof(uint32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
+  }
+  TL_CUDA(cudaStreamSynchronize(s));
+}
+
 int tl_aot_count(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
-  return guarded([&] { run_checked(og, opt, tlb::AotMode::count, stats); });
+  return guarded([&] { run_checked(og, opt, tlb::AotMode::count, false, stats); });
 }
 
 int tl_aot_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
-  return guarded([&] { run_checked(og, opt, tlb::AotMode::hash, stats); });
+  return guarded([&] { run_checked(og, opt, tlb::AotMode::hash, false, stats); });
 }
 
 int tl_aot_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap, int canonical,
                 tl_stats* stats) {
+  return guarded([&] { list_checked(og, opt, false, triples, cap, canonical, stats); });
+}
+
+int tl_run_count(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
+  return guarded([&] { run_checked(og, opt, tlb::AotMode::count, true, stats); });
+}
+
+int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
+  return guarded([&] { run_checked(og, opt, tlb::AotMode::hash, true, stats); });
+}
+
+int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap, int canonical,
+                tl_stats* stats) {
+  return guarded([&] { list_checked(og, opt, true, triples, cap, canonical, stats); });
+}
+
+// ------------------------------------------------------ sequential orders
+int tl_degeneracy_order(tl_graph* g, uint32_t* rank) {
   return guarded([&] {
-    TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
-    tl_run_options o = opt ? *opt : defaults();
-    if (o.nparts == 0) o.nparts = 1;
-    TL_REQUIRE(o.part < o.nparts, TL_EINVAL, "part must be < nparts");
-    tlb::DeviceGuard guard(og->device);
-    cudaStream_t s = pick_stream(o.stream, og->stream);
-    const bool skip = o.skip_negative_phase != 0;
-    auto key = std::make_tuple(uint32_t(skip), o.part, o.nparts);
-    auto it = og->tri_cache.find(key);
-    uint64_t expect;
-    if (it == og->tri_cache.end()) {
-      tlb::AotResult c = tlb::aot_run(*og, tlb::AotMode::count, skip, o.part, o.nparts, s, nullptr, 0);
-      expect = c.positive + c.negative;
-      og->tri_cache[key] = expect;
-    } else {
-      expect = it->second;
+    TL_REQUIRE(g && (rank || g->n == 0), TL_EINVAL, "NULL argument");
+    tlb::DeviceGuard guard(g->device);
+    const uint32_t n = g->n;
+    std::vector<uint64_t> off(uint64_t(n) + 1);
+    std::vector<uint32_t> adj(2 * g->m);
+    {
+      tlb::DBuf<uint64_t> d_off;
+      tlb::DBuf<uint32_t> d_adj;
+      tlb::graph_csr(*g, d_off, d_adj);
+      TL_CUDA(cudaMemcpyAsync(off.data(), d_off.p, sizeof(uint64_t) * off.size(), cudaMemcpyDeviceToHost, g->stream));
+      if (g->m)
+        TL_CUDA(cudaMemcpyAsync(adj.data(), d_adj.p, sizeof(uint32_t) * adj.size(), cudaMemcpyDeviceToHost,
+                                g->stream));
+      TL_CUDA(cudaStreamSynchronize(g->stream));
     }
-    tlb::DBuf<uint32_t> d_out;
-    d_out.alloc(std::max<uint64_t>(3 * expect, 3), s);
-    tlb::AotResult r = tlb::aot_run(*og, tlb::AotMode::list, skip, o.part, o.nparts, s, d_out.p, expect);
-    const uint64_t T = r.emitted;
-    TL_REQUIRE(T == r.positive + r.negative, TL_ELOGIC, "emission count disagrees with the triangle counters");
-    TL_REQUIRE(T <= expect, TL_ELOGIC, "listing emitted more triangles than the counting pass");
-    if (canonical && T) {
-      tlb::canonicalize_triples(d_out.p, T, s);
-      tlb::sort_triples(d_out.p, T, og->nb, s);
-    }
-    fill_stats(stats, r);
-    if (triples) {
-      if (cap < T) {
-        TL_CUDA(cudaStreamSynchronize(s));
-        throw tlb::TlError(TL_ECAPACITY, "output capacity " + std::to_string(cap) + " < " + std::to_string(T) +
-                                             " triangles");
-      }
-      if (T) TL_CUDA(cudaMemcpyAsync(triples, d_out.p, sizeof(uint32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
-    }
-    TL_CUDA(cudaStreamSynchronize(s));
+    tlb::degeneracy_order_host(n, off.data(), adj.data(), rank);
+  });
+}
+
+int tl_random_order(uint32_t n, uint64_t seed, uint32_t* rank) {
+  return guarded([&] {
+    TL_REQUIRE(rank || n == 0, TL_EINVAL, "NULL argument");
+    tlb::random_order_host(n, seed, rank);
   });
 }
 

@@ -44,8 +44,11 @@ struct tl_oriented {
   tlb::DBuf<uint64_t> claim_off;  // n+1, by pivot
   tlb::DBuf<uint64_t> win;        // m claim windows {begin:40 | len:23 | neg:1} into col
   tlb::DBuf<uint32_t> claim_s;    // m traversed vertex ids s | neg << 31
-  // triangle count per (skip_negative, part, nparts): sizes listing buffers
-  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
+  // forward claims (kclist3 / cf merge: pivot t traverses N+(h) for every
+  // edge t->h; grouped by t = the out-CSR itself), built on first use
+  tlb::DBuf<uint64_t> fwd_win;    // m windows {off[h] | deg+(h) << 40}
+  // emission count per (algorithm, skip_negative, part, nparts): sizes listing buffers
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
   ~tl_oriented();
 };
 
@@ -100,15 +103,29 @@ void sort_triples(uint32_t* d_triples, uint64_t count, uint32_t nb, cudaStream_t
 void canonicalize_triples(uint32_t* d_triples, uint64_t count, cudaStream_t s);
 uint64_t brute_force(tl_graph& g, DBuf<uint32_t>& out);
 
+// ---- tl_orders.cu (host: sequential by definition) ----
+void degeneracy_order_host(uint32_t n, const uint64_t* off, const uint32_t* adj, uint32_t* rank);
+void random_order_host(uint32_t n, uint64_t seed, uint32_t* rank);
+
 // ---- tl_aot.cu ----
 enum class AotMode { count = 0, hash = 1, list = 2 };
+// The reference's four kernels (engine.hpp:18), numbered as TL_ALGO_*.
+enum class Algo : uint32_t { aot = 0, cf_merge = 1, cf_hash = 2, kclist3 = 3 };
 struct AotResult {
   uint64_t positive = 0, negative = 0, executed = 0, logical = 0;
   uint64_t hash_sum = 0, hash_xor = 0, emitted = 0, tasks = 0, table_builds = 0, launches = 0;
+  // RunStats as the reference reports them for the algorithm (engine.hpp:28-36)
+  uint64_t triangles = 0, probes = 0, merge_comparisons = 0, report_positive = 0, report_negative = 0;
   float list_ms = 0.f, prep_ms = 0.f;
 };
+struct RunSpec {
+  Algo algo = Algo::aot;
+  AotMode mode = AotMode::count;
+  bool skip_negative = false;  // RunOptions::aot_skip_negative_phase (aot only)
+  bool reuse = false;          // RunOptions::cf_hash_reuse_last_table (cf-hash only)
+  uint32_t part = 0, nparts = 1;
+};
 // out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).
-AotResult aot_run(tl_oriented& og, AotMode mode, bool skip_negative, uint32_t part, uint32_t nparts,
-                  cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
+AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
 
 }  // namespace tlb
