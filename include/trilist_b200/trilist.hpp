@@ -204,6 +204,7 @@ class OrientedGraph {
     VertexOrder order;
   };
   static OrientedGraph wrap(tl_oriented* h, int device);
+  static void rewrite_lists(HostLayout& L, const LocalOrder& local);
   const HostLayout& host() const;
 
   std::shared_ptr<tl_oriented> h_;

@@ -24,6 +24,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libtrilist_b200.so")
 EXT = os.path.join(PKG, "trilist", "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
+CLI = os.path.join(PKG, "bin", "trilist")
 
 CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -86,9 +87,20 @@ def build_ext(verbose: bool = False, force: bool = False) -> str:
     return EXT
 
 
+def build_cli(verbose: bool = False, force: bool = False) -> str:
+    """The `trilist` command line (tools/trilist_main.cpp's interface)."""
+    srcs = [os.path.join(CSRC, f) for f in ("cli.cpp", "report.cpp", "facade.cpp")]
+    if force or _stale(CLI, srcs + _headers() + [LIB]):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        _run(["g++", "-O2", "-std=c++20", "-I" + INC] + srcs +
+             ["-L" + LIBDIR, "-ltrilist_b200", "-Wl,-rpath,$ORIGIN/../lib", "-o", CLI], verbose)
+    return CLI
+
+
 def build(verbose: bool = False, force: bool = False) -> None:
     build_lib(verbose, force)
     build_ext(verbose, force)
+    build_cli(verbose, force)
 
 
 if __name__ == "__main__":

@@ -314,6 +314,7 @@ const OrientedGraph::HostLayout& OrientedGraph::host() const {
       check(tl_oriented_csr(h_.get(), L->out_offsets.data(), L->out.data(), L->in_offsets.data(), L->in.data(),
                             L->order.rank.data()),
             "OrientedGraph accessors");
+    if (local_.policy != LocalOrderPolicy::rank_asc) rewrite_lists(*L, local_);
     host_ = L;
   }
   return *host_;
@@ -359,27 +360,28 @@ OrientedGraph orient(const Graph& g, const VertexOrder& order) {  // ordering.cp
   return OrientedGraph::wrap(h, g.device());
 }
 
-// The device copy stays rank-ascending; only the host accessor lists are
-// rewritten, exactly as ordering.cpp:229-266 does.
-OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local) {
-  const auto& src = g.host();
-  auto L = std::make_shared<OrientedGraph::HostLayout>(src);
+// The device copy stays rank-ascending; the host accessor lists (built on
+// first access) are rewritten exactly as ordering.cpp:229-266 does.  The
+// rewrite is a pure function of (graph, order, policy, seed), so it is applied
+// lazily and a caller that never reads the lists never pays for it.
+void OrientedGraph::rewrite_lists(HostLayout& L, const LocalOrder& local) {
+  const VertexId n = VertexId(L.order.rank.size());
   auto udeg = [&](VertexId x) {
-    return VertexId(L->out_offsets[x + 1] - L->out_offsets[x] + L->in_offsets[x + 1] - L->in_offsets[x]);
+    return VertexId(L.out_offsets[x + 1] - L.out_offsets[x] + L.in_offsets[x + 1] - L.in_offsets[x]);
   };
-  const auto& rank = L->order.rank;
+  const auto& rank = L.order.rank;
   auto fisher_yates = [](VertexId* first, VertexId* last, std::uint64_t seed) {  // ordering.cpp:23-33
     std::uint64_t state = seed;
-    auto n = std::uint64_t(last - first);
-    for (std::uint64_t i = n; i > 1; --i) {
+    auto len = std::uint64_t(last - first);
+    for (std::uint64_t i = len; i > 1; --i) {
       std::uint64_t j = std::uint64_t((static_cast<unsigned __int128>(splitmix64(state)) * i) >> 64);
       std::swap(first[i - 1], first[j]);
     }
   };
-  for (VertexId u = 0; u < g.num_vertices(); ++u) {
+  for (VertexId u = 0; u < n; ++u) {
     for (std::uint64_t side = 0; side < 2; ++side) {
-      auto& lst = side ? L->in : L->out;
-      auto& off = side ? L->in_offsets : L->out_offsets;
+      auto& lst = side ? L.in : L.out;
+      auto& off = side ? L.in_offsets : L.out_offsets;
       VertexId* b = lst.data() + off[u];
       VertexId* e = lst.data() + off[u + 1];
       switch (local.policy) {
@@ -402,8 +404,11 @@ OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local) {
       }
     }
   }
-  g.host_ = L;
+}
+
+OrientedGraph apply_local_order(OrientedGraph g, const LocalOrder& local) {
   g.local_ = local;
+  g.host_.reset();  // rebuilt from the device lists on first access
   return g;
 }
 
