@@ -62,8 +62,12 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #ifndef TL_CTA_MIN_WORK
 #define TL_CTA_MIN_WORK 65536
 #endif
+#ifndef TL_EMIT_UNROLL_LONG
+#define TL_EMIT_UNROLL_LONG TL_UNROLL_LONG
+#endif
 constexpr int kUnrollShort = TL_UNROLL;
 constexpr int kUnrollLong = TL_UNROLL_LONG;
+constexpr int kUnrollLongEmit = TL_EMIT_UNROLL_LONG;  // hash / list modes (register budget)
 #ifndef TL_WARP_CTA_THREADS
 #define TL_WARP_CTA_THREADS 256
 #endif
@@ -81,7 +85,23 @@ constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
 constexpr uint32_t kCtaWordsLg = 31 - __builtin_clz(kCtaWords);
 constexpr uint32_t kCtaHashDegMax = (1u << kCtaWordsLg) / 2;
 constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below this stay on the warp hash path
-constexpr int kEmitCap = 128;    // per-warp staging of hits (hash / list modes)
+#ifndef TL_EMIT_CAP
+#define TL_EMIT_CAP 96  // 4 CTAs/SM fit (128 hits: 3 CTAs, 32% slower at C4; tools/sweep.py)
+#endif
+#ifndef TL_EMIT_CTAS
+#define TL_EMIT_CTAS 4
+#endif
+#ifndef TL_LIST_CAP
+#define TL_LIST_CAP 96  // list mode (C2 4.9 ms vs 5.2 at 3 CTAs x 128, 6.2 at 4 x 64)
+#endif
+#ifndef TL_LIST_CTAS
+#define TL_LIST_CTAS 4
+#endif
+// per-warp staging of hits (hash / list modes)
+template <AotMode MODE>
+constexpr int emit_cap() {
+  return MODE == AotMode::list ? TL_LIST_CAP : TL_EMIT_CAP;
+}
 constexpr uint32_t kShort = 32;  // claims of at most this length are packed
 constexpr uint64_t kTaskMin = 4096;    // minimum work per warp task (adaptive: ~64 tasks per warp)
 constexpr uint64_t kCtaTaskScale = 8;  // a CTA record holds kCtaTaskScale warp tasks of work
@@ -267,7 +287,7 @@ __device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, 
   const unsigned hm = __ballot_sync(kFull, hit);
   if (hm) {
     const uint32_t k = __popc(hm);
-    if (st.ecount + k > kEmitCap) flush_emits(st, P);
+    if (st.ecount + k > emit_cap<MODE>()) flush_emits(st, P);
     if (hit) {
       const uint32_t slot = st.ebase + 12 * (st.ecount + __popc(hm & lanemask_lt()));
       st_sm(slot, a_orig);
@@ -499,13 +519,15 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
 }
 
 template <AotMode MODE, int U>
-__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count ? TL_CTAS_PER_SM : 3) k_aot(Params P) {
+__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTAS_PER_SM
+                                                          : MODE == AotMode::hash ? TL_EMIT_CTAS
+                                                                                  : TL_LIST_CTAS) k_aot(Params P) {
   __shared__ unsigned long long s_task;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
   Lane<MODE> st;
-  st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (3 * kEmitCap));
+  st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (3 * emit_cap<MODE>()));
   __syncthreads();
   // ---- phase 1: CTA records
   if (P.ncta) {
@@ -809,7 +831,12 @@ int sm_count() {
 
 template <AotMode MODE>
 size_t kernel_smem() {
-  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * kEmitCap : 0));
+  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * emit_cap<MODE>() : 0));
+}
+
+template <AotMode MODE>
+constexpr int unroll_long() {
+  return MODE == AotMode::count ? kUnrollLong : kUnrollLongEmit;
 }
 
 template <AotMode MODE>
@@ -820,7 +847,7 @@ int resident_warps() {  // warps of k_aot<MODE, *> the current device keeps resi
   if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
   TL_CUDA(cudaFuncSetAttribute(k_aot<MODE, kUnrollShort>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(kernel_smem<MODE>())));
-  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE, kUnrollLong>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TL_CUDA(cudaFuncSetAttribute(k_aot<MODE, unroll_long<MODE>()>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(kernel_smem<MODE>())));
   int per_sm = 0;
   TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aot<MODE, kUnrollShort>, kWarpThreads,
@@ -837,7 +864,7 @@ uint64_t launch_kernels(const Params& P, bool long_lists, cudaStream_t s) {
   const uint64_t want = std::max<uint64_t>(P.ncta, (P.ntasks + kWarpsPerCta - 1) / kWarpsPerCta);
   const unsigned grid = unsigned(std::min<uint64_t>(want, ctas));
   if (long_lists)
-    k_aot<MODE, kUnrollLong><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
+    k_aot<MODE, unroll_long<MODE>()><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
   else
     k_aot<MODE, kUnrollShort><<<grid, kWarpThreads, kernel_smem<MODE>(), s>>>(P);
   TL_CUDA(cudaGetLastError());

@@ -22,7 +22,7 @@ def build(specs):
 
     B.build_lib()
     os.makedirs(VDIR, exist_ok=True)
-    objs = [os.path.join(B.OBJ, f) for f in ("tl_build.o", "tl_capi.o")]
+    objs = [os.path.join(B.OBJ, f.replace(".cu", ".o")) for f in B.CU_SOURCES if f != "tl_aot.cu"]
     procs = []
     for spec in specs:
         name, _, macros = spec.partition(":")
@@ -37,13 +37,13 @@ def build(specs):
         print("built", lib)
 
 
-def run(names, config):
+def run(names, config, mode="count"):
     out = {}
     for name in names:
         lib = os.path.join(VDIR, f"lib_{name}.so")
         env = dict(os.environ, TL_LIB_PATH=lib)
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_step.py"), "--config", config,
-                            "--reps", "6"], env=env, capture_output=True, text=True)
+                            "--reps", "6", "--mode", mode], env=env, capture_output=True, text=True)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
         out[name] = line
         print(name, line, flush=True)
@@ -58,4 +58,7 @@ if __name__ == "__main__":
         cfg = "c2"
         if args and args[0] == "--config":
             cfg, args = args[1], args[2:]
-        run(args, cfg)
+        mode = "count"
+        if args and args[0] == "--mode":
+            mode, args = args[1], args[2:]
+        run(args, cfg, mode)
