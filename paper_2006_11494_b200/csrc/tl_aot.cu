@@ -198,6 +198,93 @@ struct HashProbe {  // linear probing, stores x + 1, 0 = empty
   }
 };
 
+// Two-level bitmap for spans too wide for a direct bitmap: level 1 has one
+// bit per 32-id bucket of [lmin, lmax], level 2 one 32-bit mask per occupied
+// bucket, found by rank (a u16 running count per level-1 word + popc).  A
+// miss costs one LDS like the direct bitmap; a candidate two more, with no
+// data-dependent loop.  Layout from word 0: level 1 (nbw words, the last one
+// all-zero: ids outside the window clamp into it), counts (ceil(nbw/2)
+// words), masks (one word per occupied bucket).
+struct RankProbe {
+  static constexpr bool kRangeChecked = true;
+  uint32_t bm, cnt, msk, lmin, dmax;
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const {
+    const uint32_t d = min(x - lmin, dmax), b = d >> 5, w = b >> 5;
+    const uint32_t word = ld_sm(bm + (w << 2));
+    uint32_t hit = 0;
+    if ((word >> (b & 31)) & 1u) {
+      uint16_t c;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(c) : "r"(cnt + (w << 1)));
+      const uint32_t idx = uint32_t(c) + __popc(word & ((1u << (b & 31)) - 1u));
+      hit = (ld_sm(msk + (idx << 2)) >> (d & 31)) & 1u;
+    }
+    return hit;
+  }
+  __device__ __forceinline__ bool test(uint32_t x) const { return bit(x) != 0; }
+};
+
+struct RankLayout {  // word counts of a RankProbe over `span` >= 1 ids
+  uint32_t nbw, ncw;   // level-1 words (incl. the zero guard word), count words
+  __device__ __forceinline__ explicit RankLayout(uint32_t span)
+      : nbw(((span - 1) >> 10) + 2), ncw((nbw + 1) >> 1) {}
+  __device__ __forceinline__ uint32_t words(uint32_t dl) const { return nbw + ncw + dl; }  // dl >= masks
+};
+
+__device__ __forceinline__ bool rank_fits(uint32_t dl, uint32_t span, uint32_t words) {
+  return RankLayout(span).words(dl) <= words;
+}
+
+__device__ __forceinline__ RankProbe rank_probe(uint32_t base, uint32_t lmin, uint32_t span) {
+  const RankLayout L(span);
+  RankProbe p;
+  p.bm = base;
+  p.cnt = base + 4 * L.nbw;
+  p.msk = p.cnt + 4 * L.ncw;
+  p.lmin = lmin;
+  p.dmax = (L.nbw - 1) << 10;  // first id of the all-zero last level-1 word
+  return p;
+}
+
+// Built by one warp from the sorted list nl[0, dl) into the zeroed region of
+// p (rank_probe); returns the number of mask words written.
+__device__ __forceinline__ uint32_t rank_build(const RankProbe& p, const uint32_t* nl, uint32_t dl, uint32_t span) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lmin = p.lmin;
+  const RankLayout L(span);
+  uint32_t carry = 0;  // occupied buckets so far
+  for (uint32_t i0 = 0; i0 < dl; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool valid = i < dl;
+    const uint32_t d = valid ? __ldg(nl + i) - lmin : 0u;
+    const uint32_t b = d >> 5;
+    const uint32_t pb = (valid && i > 0) ? (__ldg(nl + i - 1) - lmin) >> 5 : 0xFFFFFFFFu;
+    const bool first = valid && b != pb;
+    const unsigned fm = __ballot_sync(kFull, first);
+    const uint32_t idx = carry + __popc(fm & ((2u << lane) - 1u)) - 1u;  // this element's bucket rank
+    if (first) red_or_sm(p.bm + ((b >> 5) << 2), 1u << (b & 31));
+    if (valid) red_or_sm(p.msk + (idx << 2), 1u << (d & 31));
+    carry += __popc(fm);
+  }
+  __syncwarp();
+  // counts: exclusive prefix of popc over the level-1 words
+  const uint32_t per = (L.nbw + 31) >> 5, w0 = min(lane * per, L.nbw), w1 = min(w0 + per, L.nbw);
+  uint32_t local = 0;
+  for (uint32_t w = w0; w < w1; ++w) local += __popc(ld_sm(p.bm + (w << 2)));
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= uint32_t(o)) incl += t;
+  }
+  uint32_t run = incl - local;
+  for (uint32_t w = w0; w < w1; ++w) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(p.cnt + (w << 1)), "h"(uint16_t(run)));
+    run += __popc(ld_sm(p.bm + (w << 2)));
+  }
+  __syncwarp();
+  return carry;
+}
+
 struct GlobalProbe {  // pivots beyond every shared-memory layout
   static constexpr bool kRangeChecked = false;
   const uint32_t* list;
@@ -444,6 +531,13 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
       for (uint32_t i = lane; i < nwords; i += 32) st_sm(wbase + 4 * i, 0u);
     else
       for (uint32_t i = lane; i < R.dl; i += 32) bitmap_clear(wbase, lmin, __ldg(nl + i));
+  } else if (rank_fits(R.dl, span, kWarpWords)) {
+    const RankProbe probe = rank_probe(wbase, lmin, span);
+    const uint32_t nmask = rank_build(probe, nl, R.dl, span);
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+    __syncwarp();
+    const RankLayout L(span);
+    for (uint32_t i = lane; i < L.nbw + L.ncw + nmask; i += 32) st_sm(wbase + 4 * i, 0u);
   } else {
     uint32_t lg = 32 - __clz(4 * R.dl - 1);
     lg = max(5u, min(lg, kWarpWordsLg));
@@ -502,6 +596,14 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
       for (uint32_t i = threadIdx.x; i < nwords; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
     else
       for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) bitmap_clear(cbase, lmin, __ldg(nl + i));
+  } else if (rank_fits(R.dl, span, kCtaWords)) {
+    const RankProbe probe = rank_probe(cbase, lmin, span);
+    if (threadIdx.x < 32) rank_build(probe, nl, R.dl, span);
+    __syncthreads();
+    cta_claims<MODE, U>(P, R, probe, lmax, a_orig, st);
+    __syncthreads();
+    const RankLayout L(span);
+    for (uint32_t i = threadIdx.x; i < L.words(R.dl); i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
   } else if (R.dl <= kCtaHashDegMax) {
     uint32_t lg = 32 - __clz(2 * R.dl - 1);
     lg = max(5u, min(lg, kCtaWordsLg));
@@ -648,6 +750,8 @@ __global__ void k_logical(const uint32_t* cs, const uint64_t* off, uint64_t cb, 
 
 // Warp path: the span fits the warp bitmap, or a small pivot (warp hash) with
 // too little work to occupy a CTA.  Everything else is a phase-1 CTA record.
+// (Sending every record whose two-level bitmap fits a warp region to the
+// warp path measured the same at C2/C3/C5 and 5% slower at C4.)
 __device__ __forceinline__ bool warp_path(uint32_t dl, uint32_t span, uint64_t work) {
   return span <= kWarpSpanMax || (dl <= kWarpHashDegMax && work < kCtaMinWork);
 }
@@ -679,7 +783,7 @@ __global__ void k_classify(const uint64_t* CP, const uint64_t* claim_off, const 
 }
 
 // Diagnostic (TL_DEBUG_PATHS=1): windowed work W per probe path and per
-// log2(span) bucket.  out[0..4] = warp bitmap, warp hash, CTA bitmap, CTA
+// log2(span) bucket.  out[0..6] = warp bitmap, warp rank, warp hash, CTA bitmap, CTA rank, CTA
 // hash, global search; out[8 + b] = work with ceil(log2(span)) == b.
 __global__ void k_path_stats(const uint64_t* CP, const uint64_t* claim_off, const uint64_t* off, const uint32_t* col,
                              uint32_t pb, uint32_t np, uint64_t cb, uint64_t ce, unsigned long long* out) {
@@ -693,10 +797,11 @@ __global__ void k_path_stats(const uint64_t* CP, const uint64_t* claim_off, cons
     const uint32_t span = col[lb + dl - 1] - col[lb] + 1;
     int path;
     if (span <= kWarpSpanMax) path = 0;
-    else if (warp_path(dl, span, W + kKappa * (b - a))) path = 1;
-    else if (span <= kCtaSpanMax) path = 2;
-    else if (dl <= kCtaHashDegMax) path = 3;
-    else path = 4;
+    else if (warp_path(dl, span, W + kKappa * (b - a))) path = rank_fits(dl, span, kWarpWords) ? 1 : 2;
+    else if (span <= kCtaSpanMax) path = 3;
+    else if (rank_fits(dl, span, kCtaWords)) path = 4;
+    else if (dl <= kCtaHashDegMax) path = 5;
+    else path = 6;
     atomicAdd(out + path, (unsigned long long)W);
     atomicAdd(out + 8 + (32 - __clz(span - 1 | 1)), (unsigned long long)W);
   }
@@ -1000,8 +1105,10 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
       unsigned long long hp[48];
       TL_CUDA(cudaMemcpyAsync(hp, ps.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
       TL_CUDA(cudaStreamSynchronize(s));
-      fprintf(stderr, "[tl paths] warp-bitmap %llu warp-hash %llu cta-bitmap %llu cta-hash %llu global %llu\n", hp[0],
-              hp[1], hp[2], hp[3], hp[4]);
+      fprintf(stderr,
+              "[tl paths] warp-bitmap %llu warp-rank %llu warp-hash %llu cta-bitmap %llu cta-rank %llu cta-hash %llu "
+              "global %llu\n",
+              hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[6]);
       fprintf(stderr, "[tl span log2 buckets]");
       for (int b = 0; b < 40; ++b)
         if (hp[8 + b]) fprintf(stderr, " %d:%llu", b, hp[8 + b]);
