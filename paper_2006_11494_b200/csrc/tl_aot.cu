@@ -27,7 +27,10 @@
 //     cost-balanced tasks over consecutive records, fetched dynamically; the
 //     same cost prefix cuts the multi-GPU parts.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 
@@ -659,30 +662,19 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
 #define TL_GRID_STRIDE(i, count) \
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (count); i += uint64_t(gridDim.x) * blockDim.x)
 
-// Claim cost (window upper bound): deg+(s) - pos; 0 for skipped negative
-// claims.  With `logical`, also sums the logical probes (deg+(s) per claim).
-__global__ void k_claim_cost(const uint64_t* win, const uint32_t* cs, const uint64_t* off, uint64_t m,
-                             uint32_t skip_neg, uint64_t* cost, unsigned long long* logical) {
-  unsigned long long lsum = 0;
-  TL_GRID_STRIDE(i, m + 1) {
-    uint64_t c = 0;
-    if (i < m) {
-      const uint64_t w = win[i];
-      if (!(skip_neg && (w >> 63))) {
-        c = (w >> kWinLenShift) & kWinLenMask;
-        if (logical) {
-          const uint32_t s = cs[i] & ~kNegBit;
-          lsum += off[s + 1] - off[s];
-        }
-      }
-    }
-    cost[i] = c;
+// Claim cost (the window's length, an upper bound of its probes; 0 for a
+// skipped negative claim), for claim i < m; 0 at i = m so an exclusive scan of
+// m + 1 items ends in the total.
+struct WindowLength {
+  const uint64_t* win;
+  uint64_t m;
+  uint32_t skip_neg;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    if (i >= m) return 0;
+    const uint64_t w = win[i];
+    return (skip_neg && (w >> 63)) ? 0 : (w >> kWinLenShift) & kWinLenMask;
   }
-  if (logical) {
-    for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
-    if ((threadIdx.x & 31) == 0 && lsum) atomicAdd(logical, lsum);
-  }
-}
+};
 
 __device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t lo, uint64_t hi, uint64_t x) {
   while (lo < hi) {
@@ -1021,6 +1013,15 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     }
   } evg{ev};
   TL_CUDA(cudaEventRecord(ev[0], s));
+  // TL_DEBUG_PREP=1: host-side phase timeline of the task construction
+  const bool dbg = getenv("TL_DEBUG_PREP") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[tl prep] %-12s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
 
   DBuf<unsigned long long> acc;
   acc.alloc(kAccN, s);
@@ -1029,12 +1030,24 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   // claim-cost prefix CP[0..m]
   DBuf<uint64_t> CP;
   CP.alloc(m + 1, s);
+  mark("alloc");
   const bool whole = nparts == 1;
-  k_claim_cost<<<grid_for(m + 1, 256, 148u * 64u), 256, 0, s>>>(cwin, cs, og.off.p, m, skip_negative,
-                                                               CP.p, whole ? acc.p + kLogical : nullptr);
-  TL_CUDA(cudaGetLastError());
-  cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, CP.p, m + 1, s); });
-  r.launches += 1 + 2;  // k_claim_cost, scan (init + sweep)
+  // CP = exclusive scan of the window lengths, read straight from the packed
+  // windows (one pass: 8 B in, 8 B out per claim)
+  auto lens = thrust::make_transform_iterator(thrust::counting_iterator<uint64_t>(0), WindowLength{cwin, m, skip_negative});
+  cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, lens, CP.p, m + 1, s); });
+  r.launches += 2;  // scan (init + sweep)
+  // logical probes (engine.hpp:250/:264): the orientation's cost model when
+  // the run covers every claim, else a pass over the part's claims
+  const bool logical_from_cost = whole && !skip_negative;
+  if (logical_from_cost) {
+    r.logical = fwd ? og.cost[1] : og.cost[2];
+  } else if (whole) {
+    k_logical<<<grid_for(m, 256, 148u * 32u), 256, 0, s>>>(cs, og.off.p, 0, m, skip_negative, acc.p + kLogical);
+    TL_CUDA(cudaGetLastError());
+    ++r.launches;
+  }
+  mark("cost+scan");
   uint64_t cb = 0, ce = m;
   uint32_t pb = 0, pe = og.n;
   if (whole) {
@@ -1080,6 +1093,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     long_lists = ce > cb && (w[1] - w[0]) / (ce - cb) >= TL_LONG_WINDOW;
   }
 
+  mark("task size");
   const uint32_t np = cb < ce ? pe - pb : 0;
   DBuf<uint32_t> nrw, nrc, ow, oc;
   DBuf<Rec> wrecs, crecs;
@@ -1120,6 +1134,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     TL_CUDA(cudaStreamSynchronize(s));
     nw = tw;
     nc = tc;
+    mark("classify");
     r.launches += 1 + 2 * 2;
     if (nw) {
       wrecs.alloc(nw, s);
@@ -1146,6 +1161,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
       ++r.launches;
     }
   }
+  mark("records");
   TL_CUDA(cudaEventRecord(ev[1], s));
 
   Params P{};
@@ -1202,7 +1218,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   r.positive = h[kPos];
   r.negative = h[kNeg];
   r.executed = wce - wcb;  // probes left after the rank-window pruning of each list
-  r.logical = h[kLogical];
+  if (!logical_from_cost) r.logical = h[kLogical];
   r.hash_sum = h[kHsum];
   r.hash_xor = h[kHxor];
   r.emitted = h[kEmitted];
