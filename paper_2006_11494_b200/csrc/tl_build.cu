@@ -276,26 +276,40 @@ __global__ void k_rank_degrees(const uint32_t* orig, uint32_t n, const uint64_t*
   }
 }
 
-// Rows of the reference layout (original ids) -> rank-space directed keys.
+// Rows of the reference layout (original ids) -> rank-space directed keys at
+// each row's rank position.  Eight lanes per row, so reads and writes of a
+// row are coalesced (rows average ~16 entries at the BASELINE configs).
 // flags: bit0 = some row not rank-ascending, bit1 = an edge against the order
 // or an id out of range.
 __global__ void k_rows_to_keys(const uint64_t* out_off, const uint32_t* out, const uint32_t* rank, uint32_t n,
                                uint32_t nb, const uint64_t* off, uint64_t* dk, uint32_t* flags) {
-  TL_GRID_STRIDE(u, uint64_t(n)) {
-    uint32_t t = rank[u];
-    uint64_t src = out_off[u], len = out_off[u + 1] - src, dst = off[t];
-    uint32_t prev = t;
-    uint32_t f = 0;
-    for (uint64_t j = 0; j < len; ++j) {
-      uint32_t v = out[src + j];
-      uint32_t h = v < n ? rank[v] : 0;
-      if (v >= n || h <= t) f |= 2u;
-      if (h <= prev) f |= 1u;
-      prev = h;
-      dk[dst + j] = (uint64_t(t) << nb) | h;
+  constexpr uint32_t G = 8;
+  const uint32_t gl = threadIdx.x & (G - 1);
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+  const uint64_t groups = (uint64_t(gridDim.x) * blockDim.x) / G;
+  uint32_t f = 0;
+  for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G; u < n; u += groups) {
+    const uint32_t t = rank[u];
+    const uint64_t src = out_off[u], len = out_off[u + 1] - src, dst = off[t];
+    uint32_t carry = t;  // rank of the previous entry (the tail before the first)
+    for (uint64_t j0 = 0; j0 < len; j0 += G) {
+      const uint64_t j = j0 + gl;
+      const bool valid = j < len;
+      uint32_t h = 0;
+      if (valid) {
+        const uint32_t v = out[src + j];
+        h = v < n ? rank[v] : 0;
+        if (v >= n || h <= t) f |= 2u;
+        dk[dst + j] = (uint64_t(t) << nb) | h;
+      }
+      uint32_t prev = __shfl_up_sync(gmask, h, 1, G);
+      if (gl == 0) prev = carry;
+      if (valid && h <= prev) f |= 1u;
+      const uint32_t last = uint32_t(len - j0 < G ? len - j0 - 1 : G - 1);
+      carry = __shfl_sync(gmask, h, last, G);
     }
-    if (f) atomicOr(flags, f);
   }
+  if (f) atomicOr(flags, f);
 }
 
 __global__ void k_orig_degrees(const uint32_t* rank, uint32_t n, const uint64_t* off, uint64_t* deg) {
@@ -707,7 +721,7 @@ void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* 
   flags.alloc(1, s);
   TL_CUDA(cudaMemsetAsync(flags.p, 0, 4, s));
   if (m) {
-    k_rows_to_keys<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_out_off, d_out, og.rank.p, n, og.nb, og.off.p, dk.p,
+    k_rows_to_keys<<<grid_for(uint64_t(n) * 8, kBlock, 148u * 64u), kBlock, 0, s>>>(d_out_off, d_out, og.rank.p, n, og.nb, og.off.p, dk.p,
                                                           flags.p);
     TL_CUDA(cudaGetLastError());
   }
