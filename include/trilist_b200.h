@@ -179,6 +179,34 @@ TL_API int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* sta
 TL_API int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
                        int canonical, tl_stats* stats);
 
+/* verify_equivalence's comparison (engine.cpp:82-130) for one orientation,
+ * on the device: every algorithm in `algorithms` (TL_ALGO_*) lists its
+ * emissions, which are canonicalised, sorted and de-duplicated on the device
+ * and compared with the baseline by device set differences -- the oracle's
+ * triples `reference` (host, any order, sorted and de-duplicated here) when
+ * have_reference != 0, else the first algorithm's set.  opt carries the
+ * RunOptions (skip_negative_phase, cf_hash_reuse_last_table, stream);
+ * opt->algorithm is ignored.  results[nalgos]; reference_count = size of the
+ * baseline set.  Only counters and the first TL_VERIFY_SAMPLES differences of
+ * each side leave the device. */
+#define TL_VERIFY_SAMPLES 32 /* VerifyReport::kMaxSamples (engine.hpp:362) */
+typedef struct tl_verify_result {
+  uint32_t algorithm; /* TL_ALGO_* */
+  uint32_t pass;
+  uint64_t unique_triangles;
+  uint64_t duplicate_emissions;
+  uint64_t missing_count; /* in the baseline, not emitted */
+  uint64_t extra_count;   /* emitted, not in the baseline */
+  uint32_t n_missing_samples;
+  uint32_t n_extra_samples;
+  uint32_t missing_samples[3 * TL_VERIFY_SAMPLES]; /* sorted canonical triples */
+  uint32_t extra_samples[3 * TL_VERIFY_SAMPLES];
+  tl_stats stats;
+} tl_verify_result;
+TL_API int tl_verify(tl_oriented* og, const uint32_t* algorithms, uint32_t nalgos, const tl_run_options* opt,
+                     const uint32_t* reference, uint64_t nreference, int have_reference,
+                     tl_verify_result* results, uint64_t* reference_count);
+
 /* degeneracy_order / random_order -- ordering.cpp:86-120.  The degeneracy
  * order removes, one vertex at a time, the vertex of least (current degree,
  * id) -- an inherently sequential chain -- and random_order is a Fisher-Yates

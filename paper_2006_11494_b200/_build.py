@@ -26,7 +26,7 @@ LIB = os.path.join(LIBDIR, "libtrilist_b200.so")
 EXT = os.path.join(PKG, "trilist", "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 CLI = os.path.join(PKG, "bin", "trilist")
 
-CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_capi.cu"]
+CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_verify.cu", "tl_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -26,7 +26,8 @@ EXPORTS = (
     "tl_graph_from_pairs", "tl_graph_free", "tl_graph_info", "tl_graph_degrees", "tl_graph_csr",
     "tl_graph_from_text", "tl_graph_from_file", "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
     "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list",
-    "tl_run_count", "tl_run_hash", "tl_run_list", "tl_degeneracy_order", "tl_random_order", "tl_brute_force",
+    "tl_run_count", "tl_run_hash", "tl_run_list", "tl_verify", "tl_degeneracy_order", "tl_random_order",
+    "tl_brute_force",
 )
 
 # TL_ALGO_* (Algorithm, engine.hpp:18) by the reference's names (engine.cpp:7-15).
@@ -43,6 +44,26 @@ class TlStats(C.Structure):
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+VERIFY_SAMPLES = 32  # TL_VERIFY_SAMPLES
+
+
+class TlVerifyResult(C.Structure):
+    _fields_ = [("algorithm", C.c_uint32), ("pass_", C.c_uint32), ("unique_triangles", C.c_uint64),
+                ("duplicate_emissions", C.c_uint64), ("missing_count", C.c_uint64), ("extra_count", C.c_uint64),
+                ("n_missing_samples", C.c_uint32), ("n_extra_samples", C.c_uint32),
+                ("missing_samples", C.c_uint32 * (3 * VERIFY_SAMPLES)),
+                ("extra_samples", C.c_uint32 * (3 * VERIFY_SAMPLES)), ("stats", TlStats)]
+
+    def as_dict(self) -> dict:
+        names = {v: k for k, v in ALGO_CODES.items()}
+        ms = [tuple(self.missing_samples[3 * i:3 * i + 3]) for i in range(self.n_missing_samples)]
+        es = [tuple(self.extra_samples[3 * i:3 * i + 3]) for i in range(self.n_extra_samples)]
+        return {"algorithm": names[self.algorithm], "pass": bool(self.pass_),
+                "unique_triangles": self.unique_triangles, "duplicate_emissions": self.duplicate_emissions,
+                "missing_count": self.missing_count, "extra_count": self.extra_count,
+                "missing_samples": ms, "extra_samples": es, "stats": self.stats.as_dict()}
 
 
 class TlLoadDiag(C.Structure):
@@ -110,6 +131,8 @@ def lib() -> C.CDLL:
     L.tl_run_count.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_run_hash.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_run_list.argtypes = [vp, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int, C.POINTER(TlStats)]
+    L.tl_verify.argtypes = [vp, u32p, C.c_uint32, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int,
+                            C.POINTER(TlVerifyResult), u64p]
     L.tl_degeneracy_order.argtypes = [vp, u32p]
     L.tl_random_order.argtypes = [C.c_uint32, C.c_uint64, u32p]
     L.tl_brute_force.argtypes = [vp, C.c_uint32, u32p, C.c_uint64, u64p]
@@ -324,6 +347,18 @@ class DeviceOriented:
         c = np.zeros(3, np.uint64)
         _check(lib().tl_cost_model(self._h, _p64(c)))
         return dict(cf_cost=int(c[0]), kclist_cost=int(c[1]), aot_cost=int(c[2]))
+
+    def verify(self, algos=("cf", "cf-hash", "kclist", "aot"), reference=None, skip_negative=False, reuse=False,
+               stream=0):
+        """tl_verify: (per-algorithm result dicts, baseline size)."""
+        codes = np.array([ALGO_CODES[a] for a in algos], np.uint32)
+        res = (TlVerifyResult * max(len(algos), 1))()
+        cnt = np.zeros(1, np.uint64)
+        o = run_options(skip_negative, 0, 1, stream, "aot", reuse)
+        ref = None if reference is None else np.ascontiguousarray(reference, np.uint32).reshape(-1, 3)
+        _check(lib().tl_verify(self._h, _p32(codes), len(algos), C.byref(o), _p32(ref) if ref is not None else None,
+                               0 if ref is None else ref.shape[0], int(ref is not None), res, _p64(cnt)))
+        return [res[i].as_dict() for i in range(len(algos))], int(cnt[0])
 
     # algo="aot" goes through tl_aot_*, the others through tl_run_* (TL_ALGO_*).
     def count(self, skip_negative=False, part=0, nparts=1, stream=0, algo="aot", reuse=False) -> dict:

@@ -592,42 +592,9 @@ std::vector<Triangle> canonicalize_emissions(std::span<const std::array<VertexId
   return out;
 }
 
-namespace {
-void diff_sets(const std::vector<Triangle>& reference, const std::vector<Triangle>& got,
-               VerifyAlgorithmResult& r) {  // engine.cpp:62-78
-  std::size_t i = 0, j = 0;
-  while (i < reference.size() || j < got.size()) {
-    if (j == got.size() || (i < reference.size() && reference[i] < got[j])) {
-      if (r.missing_samples.size() < VerifyReport::kMaxSamples) r.missing_samples.push_back(reference[i]);
-      ++r.missing_count, ++i;
-    } else if (i == reference.size() || got[j] < reference[i]) {
-      if (r.extra_samples.size() < VerifyReport::kMaxSamples) r.extra_samples.push_back(got[j]);
-      ++r.extra_count, ++j;
-    } else {
-      ++i, ++j;
-    }
-  }
-}
-
-// Device-canonicalised, device-sorted emission list (duplicates kept).
-std::vector<Triangle> device_canonical(Algorithm algo, const OrientedGraph& g, const RunOptions& opt,
-                                       RunStats& stats) {
-  std::vector<Triangle> out;
-  if (!g.handle()) return out;
-  tl_run_options o = detail::options_for(algo, opt);
-  tl_stats s;
-  check(tl_run_list(g.handle(), &o, nullptr, 0, 1, &s), "list run");
-  out.resize(s.triangles);
-  static_assert(sizeof(Triangle) == 12, "Triangle layout");
-  check(tl_run_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(out.data()), out.size(), 1, &s), "list run");
-  stats = detail::to_run_stats(s);
-  return out;
-}
-}  // namespace
-
 VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algorithms, const VertexOrder& order,
                                 const LocalOrder& local, const std::vector<Triangle>* reference,
-                                const RunOptions& opt) {  // engine.cpp:82-130
+                                const RunOptions& opt) {  // engine.cpp:82-130, compared on the device (tl_verify)
   for (Algorithm a : algorithms) detail::require_device_algorithm(a);
   OrientedGraph oriented = orient(g, order);
   // cf runs on the rank-ascending layout it requires, the others on `local`;
@@ -635,31 +602,46 @@ VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algor
   // (test_engine.cpp:172-185), so every run uses the device's lists.
   (void)local;
   VerifyReport report;
-  std::vector<Triangle> baseline;
-  if (reference) {
-    baseline = *reference;
-    std::sort(baseline.begin(), baseline.end());
-    baseline.erase(std::unique(baseline.begin(), baseline.end()), baseline.end());
-    report.reference = "oracle";
-  }
-  for (Algorithm algo : algorithms) {
-    VerifyAlgorithmResult r;
-    r.algorithm = algo;
-    std::vector<Triangle> canon = device_canonical(algo, oriented, opt, r.stats);
-    std::vector<Triangle> uniq = canon;
-    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    r.unique_triangles = uniq.size();
-    r.duplicate_emissions = canon.size() - uniq.size();
-    if (!reference && report.results.empty()) {
-      baseline = uniq;
-      report.reference = to_string(algo);
+  report.reference = reference ? "oracle" : (algorithms.empty() ? "" : to_string(algorithms.front()));
+  if (!oriented.handle()) {  // empty graph: every set is empty
+    for (Algorithm a : algorithms) {
+      VerifyAlgorithmResult r;
+      r.algorithm = a;
+      report.results.push_back(r);
     }
-    diff_sets(baseline, uniq, r);
-    r.pass = r.duplicate_emissions == 0 && r.missing_count == 0 && r.extra_count == 0;
+    return report;
+  }
+  std::vector<std::uint32_t> codes;
+  for (Algorithm a : algorithms) codes.push_back(detail::algorithm_code(a));
+  tl_run_options o = detail::options_for(Algorithm::aot, opt);
+  std::vector<tl_verify_result> res(codes.size());
+  std::uint64_t ref_count = 0;
+  static_assert(sizeof(Triangle) == 12, "Triangle layout");
+  check(tl_verify(oriented.handle(), codes.data(), std::uint32_t(codes.size()), &o,
+                  reference ? reinterpret_cast<const std::uint32_t*>(reference->data()) : nullptr,
+                  reference ? reference->size() : 0, reference ? 1 : 0, res.data(), &ref_count),
+        "verify_equivalence");
+  auto samples = [](const std::uint32_t* t, std::uint32_t k) {
+    std::vector<Triangle> v;
+    for (std::uint32_t i = 0; i < k; ++i) v.push_back({t[3 * i], t[3 * i + 1], t[3 * i + 2]});
+    return v;
+  };
+  for (std::size_t i = 0; i < res.size(); ++i) {
+    const tl_verify_result& x = res[i];
+    VerifyAlgorithmResult r;
+    r.algorithm = algorithms[i];
+    r.stats = detail::to_run_stats(x.stats);
+    r.unique_triangles = x.unique_triangles;
+    r.duplicate_emissions = x.duplicate_emissions;
+    r.missing_count = x.missing_count;
+    r.extra_count = x.extra_count;
+    r.missing_samples = samples(x.missing_samples, x.n_missing_samples);
+    r.extra_samples = samples(x.extra_samples, x.n_extra_samples);
+    r.pass = x.pass != 0;
     report.pass = report.pass && r.pass;
     report.results.push_back(std::move(r));
   }
-  report.reference_count = baseline.size();
+  report.reference_count = ref_count;
   return report;
 }
 

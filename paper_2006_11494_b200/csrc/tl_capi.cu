@@ -49,7 +49,18 @@ void require_device(int device) {
 
 cudaStream_t pick_stream(void* user, cudaStream_t own) { return user ? static_cast<cudaStream_t>(user) : own; }
 
-void fill_stats(tl_stats* st, const tlb::AotResult& r) {
+tl_run_options defaults() {
+  tl_run_options o;
+  std::memset(&o, 0, sizeof(o));
+  o.nparts = 1;
+  return o;
+}
+
+}  // namespace
+
+namespace tlb {
+
+void fill_stats_from(const AotResult& r, tl_stats* st) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));
   st->triangles = r.triangles;
@@ -66,17 +77,6 @@ void fill_stats(tl_stats* st, const tlb::AotResult& r) {
   st->prep_ms = r.prep_ms;
   st->kernel_launches = r.launches;
 }
-
-tl_run_options defaults() {
-  tl_run_options o;
-  std::memset(&o, 0, sizeof(o));
-  o.nparts = 1;
-  return o;
-}
-
-}  // namespace
-
-namespace tlb {
 
 void ensure_device_setup(int device) {
   static std::mutex mu;
@@ -445,7 +445,7 @@ static void run_checked(tl_oriented* og, const tl_run_options* opt, tlb::AotMode
   tlb::DeviceGuard guard(og->device);
   tlb::AotResult r = tlb::aot_run(*og, sp, pick_stream(o.stream, og->stream), nullptr, 0);
   og->tri_cache[cache_key(sp)] = r.triangles;
-  fill_stats(stats, r);
+  tlb::fill_stats_from(r, stats);
 }
 
 static void list_checked(tl_oriented* og, const tl_run_options* opt, bool any_algorithm, uint32_t* triples,
@@ -476,7 +476,7 @@ static void list_checked(tl_oriented* og, const tl_run_options* opt, bool any_al
     tlb::canonicalize_triples(d_out.p, T, s);
     tlb::sort_triples(d_out.p, T, og->nb, s);
   }
-  fill_stats(stats, r);
+  tlb::fill_stats_from(r, stats);
   if (triples) {
     if (cap < T) {
       TL_CUDA(cudaStreamSynchronize(s));
@@ -512,6 +512,25 @@ int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
 int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap, int canonical,
                 tl_stats* stats) {
   return guarded([&] { list_checked(og, opt, true, triples, cap, canonical, stats); });
+}
+
+int tl_verify(tl_oriented* og, const uint32_t* algorithms, uint32_t nalgos, const tl_run_options* opt,
+              const uint32_t* reference, uint64_t nreference, int have_reference, tl_verify_result* results,
+              uint64_t* reference_count) {
+  return guarded([&] {
+    TL_REQUIRE(og && (algorithms || nalgos == 0) && (results || nalgos == 0), TL_EINVAL, "NULL argument");
+    TL_REQUIRE(!have_reference || reference || nreference == 0, TL_EINVAL, "NULL reference");
+    for (uint32_t i = 0; i < nalgos; ++i)
+      TL_REQUIRE(algorithms[i] <= TL_ALGO_KCLIST3, TL_EINVAL, "unknown algorithm " + std::to_string(algorithms[i]));
+    tl_run_options o = opt ? *opt : defaults();
+    o.algorithm = 0;
+    o.part = 0;
+    o.nparts = 1;
+    tlb::RunSpec sp = spec_of(o, tlb::AotMode::count, true);
+    tlb::DeviceGuard guard(og->device);
+    tlb::verify_algorithms(*og, algorithms, nalgos, sp, reference, nreference, have_reference != 0,
+                           pick_stream(o.stream, og->stream), results, reference_count);
+  });
 }
 
 // ------------------------------------------------------ sequential orders

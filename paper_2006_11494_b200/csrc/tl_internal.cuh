@@ -127,5 +127,11 @@ struct RunSpec {
 };
 // out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).
 AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
+void fill_stats_from(const AotResult& r, tl_stats* st);  // tl_capi.cu
+
+// ---- tl_verify.cu ----
+void verify_algorithms(tl_oriented& og, const uint32_t* algos, uint32_t nalgos, const RunSpec& base,
+                       const uint32_t* h_reference, uint64_t nreference, bool have_reference, cudaStream_t s,
+                       tl_verify_result* results, uint64_t* reference_count);
 
 }  // namespace tlb
