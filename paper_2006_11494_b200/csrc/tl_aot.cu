@@ -94,6 +94,12 @@ constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below thi
 #ifndef TL_EMIT_CTAS
 #define TL_EMIT_CTAS 4
 #endif
+#ifndef TL_CTA_TAIL
+#define TL_CTA_TAIL 2048  // C5 -2.7%, C4 -0.8%, C4 hash -1.7% (tools/sweep.py)
+#endif
+#ifndef TL_CTA_TAIL_BS
+#define TL_CTA_TAIL_BS 8
+#endif
 #ifndef TL_LIST_CAP
 #define TL_LIST_CAP 96  // list mode (C2 4.9 ms vs 5.2 at 3 CTAs x 128, 6.2 at 4 x 64)
 #endif
@@ -107,7 +113,10 @@ constexpr int emit_cap() {
 }
 constexpr uint32_t kShort = 32;  // claims of at most this length are packed
 constexpr uint64_t kTaskMin = 4096;    // minimum work per warp task (adaptive: ~64 tasks per warp)
-constexpr uint64_t kCtaTaskScale = 8;  // a CTA record holds kCtaTaskScale warp tasks of work
+#ifndef TL_CTA_TASK_SCALE
+#define TL_CTA_TASK_SCALE 8
+#endif
+constexpr uint64_t kCtaTaskScale = TL_CTA_TASK_SCALE;  // a CTA record holds kCtaTaskScale warp tasks of work
 constexpr uint64_t kBeta = 2;    // staging weight per N+(l) element
 constexpr uint64_t kGamma = 64;  // per-record overhead
 constexpr uint64_t kKappa = 8;   // per-claim overhead (scheduling and the multi-GPU cut)
@@ -573,11 +582,18 @@ __device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const 
                                            uint32_t a_orig, Lane<MODE>& st) {
   unsigned long long* cur = cta_cursor();
   while (true) {
-    unsigned long long base = 0;
-    if (lane_id() == 0) base = atomicAdd(cur, 32ull);
+    // batches of 32 claims, then of TL_CTA_TAIL_BS once fewer than
+    // TL_CTA_TAIL remain: the closing barrier waits for at most a short batch
+    unsigned long long base = 0, bs = 32;
+    if (lane_id() == 0) {
+      const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(cur);
+      if (c + TL_CTA_TAIL >= R.ce) bs = TL_CTA_TAIL_BS;
+      base = atomicAdd(cur, bs);
+    }
     base = __shfl_sync(kFull, base, 0);
+    bs = __shfl_sync(kFull, bs, 0);
     if (base >= R.ce) break;
-    claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+    claim_batch<MODE, U>(P, probe, lmax, a_orig, base, min(uint64_t(base + bs), R.ce), st);
   }
 }
 
