@@ -97,10 +97,39 @@ def build_cli(verbose: bool = False, force: bool = False) -> str:
     return CLI
 
 
+VARIANTS = {
+    # Small probe regions and a low CTA threshold: small test graphs then
+    # reach every probe path (warp/CTA bitmap, rank bitmap, hash, global
+    # search) -- tests/test_gpu_paths.py runs the parity checks against it.
+    "paths": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024"],
+    "paths_hash": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024", "TL_RANK_PROBE=0",
+                   "TL_CTA_HASH_DEG=16"],  # hashes + global search
+}
+
+
+def build_variant(name: str, verbose: bool = False, force: bool = False) -> str:
+    """lib/variants/lib_<name>.so: the library with tl_aot.cu compiled under
+    VARIANTS[name]'s macros (the other objects shared with build_lib)."""
+    build_lib(verbose)
+    vdir = os.path.join(LIBDIR, "variants")
+    os.makedirs(vdir, exist_ok=True)
+    out = os.path.join(vdir, f"lib_{name}.so")
+    src = os.path.join(CSRC, "tl_aot.cu")
+    if force or _stale(out, [src] + _headers() + [LIB]):
+        o = os.path.join(OBJ, f"tl_aot_{name}.o")
+        _run([NVCC] + NVCC_FLAGS + ["-D" + d for d in VARIANTS[name]] + ["-c", src, "-o", o], verbose)
+        objs = [os.path.join(OBJ, f.replace(".cu", ".o")) for f in CU_SOURCES if f != "tl_aot.cu"]
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out, o] + objs +
+             ["-Xlinker", "--exclude-libs,ALL", "-lz"], verbose)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False) -> None:
     build_lib(verbose, force)
     build_ext(verbose, force)
     build_cli(verbose, force)
+    for name in VARIANTS:
+        build_variant(name, verbose, force)
 
 
 if __name__ == "__main__":

@@ -86,7 +86,10 @@ constexpr uint32_t kWarpStride = kWarpWords + 32;    // + an always-zero guard w
 constexpr uint32_t kCtaWords = kWarpsPerCta * kWarpStride - 32;
 constexpr uint32_t kCtaSpanMax = kCtaWords * 32;
 constexpr uint32_t kCtaWordsLg = 31 - __builtin_clz(kCtaWords);
-constexpr uint32_t kCtaHashDegMax = (1u << kCtaWordsLg) / 2;
+#ifndef TL_CTA_HASH_DEG
+#define TL_CTA_HASH_DEG ((1u << kCtaWordsLg) / 2)
+#endif
+constexpr uint32_t kCtaHashDegMax = TL_CTA_HASH_DEG;  // larger pivots use the global binary search
 constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below this stay on the warp hash path
 #ifndef TL_EMIT_CAP
 #define TL_EMIT_CAP 96  // 4 CTAs/SM fit (128 hits: 3 CTAs, 32% slower at C4; tools/sweep.py)
@@ -242,8 +245,11 @@ struct RankLayout {  // word counts of a RankProbe over `span` >= 1 ids
   __device__ __forceinline__ uint32_t words(uint32_t dl) const { return nbw + ncw + dl; }  // dl >= masks
 };
 
+#ifndef TL_RANK_PROBE
+#define TL_RANK_PROBE 1  // 0: wide windows go straight to the hash / global search (path tests)
+#endif
 __device__ __forceinline__ bool rank_fits(uint32_t dl, uint32_t span, uint32_t words) {
-  return RankLayout(span).words(dl) <= words;
+  return TL_RANK_PROBE && RankLayout(span).words(dl) <= words;
 }
 
 __device__ __forceinline__ RankProbe rank_probe(uint32_t base, uint32_t lmin, uint32_t span) {

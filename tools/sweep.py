@@ -27,7 +27,7 @@ def build(specs):
     for spec in specs:
         name, _, macros = spec.partition(":")
         defs = ["-D" + m for m in macros.split(",") if m]
-        o = os.path.join(VDIR, f"tl_aot_{name}.o")
+        o = os.path.join(B.OBJ, f"tl_aot_sweep_{name}.o")
         cmd = [B.NVCC] + B.NVCC_FLAGS + defs + ["-c", os.path.join(B.CSRC, "tl_aot.cu"), "-o", o]
         procs.append((subprocess.Popen(cmd), name, o))
     for p, name, o in procs:
