@@ -1049,16 +1049,27 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   acc.alloc(kAccN, s);
   TL_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long) * kAccN, s));
 
-  // claim-cost prefix CP[0..m]
-  DBuf<uint64_t> CP;
-  CP.alloc(m + 1, s);
+  // claim-cost prefix CP[0..m]: the exclusive scan of the window lengths,
+  // read straight from the packed windows.  A function of the orientation's
+  // claims alone (like the claims, built once): kept on the handle for the
+  // claim set / fault flag it was built for.
+  const uint32_t cp_key = (uint32_t(fwd) << 1) | uint32_t(skip_negative);
+  if (!og.cp.p || og.cp_key != cp_key) {
+    og.cp.reset();
+    og.cp.alloc(m + 1, og.stream);  // owned by the handle's stream
+    TL_CUDA(cudaStreamSynchronize(og.stream));
+    auto lens =
+        thrust::make_transform_iterator(thrust::counting_iterator<uint64_t>(0), WindowLength{cwin, m, skip_negative});
+    uint64_t* dst = og.cp.p;
+    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, lens, dst, m + 1, s); });
+    og.cp_key = cp_key;
+    r.launches += 2;  // scan (init + sweep)
+  }
+  struct {
+    const uint64_t* p;
+  } CP{og.cp.p};
   mark("alloc");
   const bool whole = nparts == 1;
-  // CP = exclusive scan of the window lengths, read straight from the packed
-  // windows (one pass: 8 B in, 8 B out per claim)
-  auto lens = thrust::make_transform_iterator(thrust::counting_iterator<uint64_t>(0), WindowLength{cwin, m, skip_negative});
-  cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, lens, CP.p, m + 1, s); });
-  r.launches += 2;  // scan (init + sweep)
   // logical probes (engine.hpp:250/:264): the orientation's cost model when
   // the run covers every claim, else a pass over the part's claims
   const bool logical_from_cost = whole && !skip_negative;

@@ -112,6 +112,7 @@ tl_oriented::~tl_oriented() {
   win.reset();
   claim_s.reset();
   fwd_win.reset();  // every buffer is freed on its stream before the stream goes
+  cp.reset();
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

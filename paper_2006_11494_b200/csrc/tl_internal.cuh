@@ -47,6 +47,10 @@ struct tl_oriented {
   // forward claims (kclist3 / cf merge: pivot t traverses N+(h) for every
   // edge t->h; grouped by t = the out-CSR itself), built on first use
   tlb::DBuf<uint64_t> fwd_win;    // m windows {off[h] | deg+(h) << 40}
+  // claim-cost prefix (m+1) of the last claim set used (aot_run), key =
+  // forward << 1 | skip_negative
+  tlb::DBuf<uint64_t> cp;
+  uint32_t cp_key = ~0u;
   // emission count per (algorithm, skip_negative, part, nparts): sizes listing buffers
   std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
   ~tl_oriented();
