@@ -103,7 +103,9 @@ VARIANTS = {
     # search) -- tests/test_gpu_paths.py runs the parity checks against it.
     "paths": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024"],
     "paths_hash": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024", "TL_RANK_PROBE=0",
-                   "TL_CTA_HASH_DEG=16"],  # hashes + global search
+                   "TL_CTA_HASH_DEG=16", "TL_BUCKET_PROBE=0"],  # linear-probing hashes + global search
+    "paths_fallback": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024", "TL_RANK_PROBE=0",
+                       "TL_BUCKET_FORCE_FAIL=1"],  # bucket hashes that fail and fall back
 }
 
 

@@ -33,6 +33,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "tl_internal.cuh"
 
@@ -103,6 +104,9 @@ constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below thi
 #ifndef TL_CTA_TAIL_BS
 #define TL_CTA_TAIL_BS 8
 #endif
+#ifndef TL_BUCKET_PROBE
+#define TL_BUCKET_PROBE 1
+#endif
 #ifndef TL_LIST_CAP
 #define TL_LIST_CAP 96  // list mode (C2 4.9 ms vs 5.2 at 3 CTAs x 128, 6.2 at 4 x 64)
 #endif
@@ -141,7 +145,9 @@ struct Params {
   const uint32_t* orig;
   const Rec* recs;      // phase 2 (warp) records
   const uint2* tasks;   // phase 2: [rb, re) record ranges
-  uint64_t ntasks;
+  uint64_t ntasks;       // this part's warp tasks: global index gtasks - 1 - (toff + t * tstride)
+  uint64_t gtasks;
+  uint32_t toff, tstride;
   const Rec* crecs;     // phase 1 (CTA) records, one per task
   uint64_t ncta;
   uint32_t skip_neg;
@@ -301,6 +307,52 @@ __device__ __forceinline__ uint32_t rank_build(const RankProbe& p, const uint32_
   }
   __syncwarp();
   return carry;
+}
+
+// Two-choice bucketized hash for small pivots with windows too wide for the
+// rank bitmap: buckets of four slots (x + 1 stored, 0 = empty), each id in one
+// of two buckets, so a lookup is two 16-byte LDS and eight compares with no
+// data-dependent loop (the linear-probing hash's probe loops diverge the warp).
+// Load <= 1/2; an insertion that finds both buckets full reports failure and
+// the record falls back to the linear-probing hash.
+__device__ __forceinline__ uint32_t bslot1(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
+__device__ __forceinline__ uint32_t bslot2(uint32_t x, uint32_t shift) { return (x * 0x85EBCA77u) >> shift; }
+__device__ __forceinline__ uint4 ld_sm4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+struct BucketProbe {
+  static constexpr bool kRangeChecked = false;
+  uint32_t base, shift;  // 2^(32 - shift) buckets of 16 bytes at byte address base
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const { return test(x); }
+  __device__ __forceinline__ bool test(uint32_t x) const {
+    const uint32_t key = x + 1;
+    const uint4 a = ld_sm4(base + (bslot1(x, shift) << 4)), b = ld_sm4(base + (bslot2(x, shift) << 4));
+    return (a.x == key) | (a.y == key) | (a.z == key) | (a.w == key) | (b.x == key) | (b.y == key) |
+           (b.z == key) | (b.w == key);
+  }
+};
+
+// lg = log2(buckets) for dl ids at load <= 1/2 (at least 8 buckets)
+__device__ __forceinline__ uint32_t bucket_lg(uint32_t dl) { return max(3u, 32u - __clz(max(dl, 2u) / 2u - 1u | 1u)); }
+
+// Inserts x (any thread set may call it concurrently); false if both of its
+// buckets are full.
+#ifndef TL_BUCKET_FORCE_FAIL
+#define TL_BUCKET_FORCE_FAIL 0  // path tests: report some insertions as failed
+#endif
+__device__ __forceinline__ bool bucket_insert(uint32_t base, uint32_t shift, uint32_t x) {
+  const uint32_t key = x + 1;
+  if (TL_BUCKET_FORCE_FAIL && x % 7 == 3) return false;
+  const uint32_t b1 = base + (bslot1(x, shift) << 4), b2 = base + (bslot2(x, shift) << 4);
+#pragma unroll
+  for (uint32_t k = 0; k < 8; ++k) {
+    const uint32_t a = (k < 4 ? b1 : b2) + 4 * (k & 3);
+    if (cas_sm(a, 0u, key) == 0u) return true;
+  }
+  return false;
 }
 
 struct GlobalProbe {  // pivots beyond every shared-memory layout
@@ -557,15 +609,33 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
     const RankLayout L(span);
     for (uint32_t i = lane; i < L.nbw + L.ncw + nmask; i += 32) st_sm(wbase + 4 * i, 0u);
   } else {
-    uint32_t lg = 32 - __clz(4 * R.dl - 1);
-    lg = max(5u, min(lg, kWarpWordsLg));
-    const uint32_t cap = 1u << lg;
-    for (uint32_t i = lane; i < R.dl; i += 32) hash_insert(wbase, cap - 1, 32 - lg, __ldg(nl + i));
-    __syncwarp();
-    const HashProbe probe{wbase, cap - 1, 32 - lg};
-    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
-    __syncwarp();
-    for (uint32_t i = lane; i < cap; i += 32) st_sm(wbase + 4 * i, 0u);
+    bool done = false;
+    const uint32_t blg = bucket_lg(R.dl);
+    if (TL_BUCKET_PROBE && (4u << blg) <= kWarpWords) {
+      bool ok = true;
+      for (uint32_t i = lane; i < R.dl; i += 32) ok &= bucket_insert(wbase, 32 - blg, __ldg(nl + i));
+      done = __all_sync(kFull, ok);
+      if (done) {
+        const BucketProbe probe{wbase, 32 - blg};
+        for (uint64_t base = R.cb; base < R.ce; base += 32)
+          claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < (4u << blg); i += 32) st_sm(wbase + 4 * i, 0u);
+      __syncwarp();
+    }
+    if (!done) {
+      uint32_t lg = 32 - __clz(4 * R.dl - 1);
+      lg = max(5u, min(lg, kWarpWordsLg));
+      const uint32_t cap = 1u << lg;
+      for (uint32_t i = lane; i < R.dl; i += 32) hash_insert(wbase, cap - 1, 32 - lg, __ldg(nl + i));
+      __syncwarp();
+      const HashProbe probe{wbase, cap - 1, 32 - lg};
+      for (uint64_t base = R.cb; base < R.ce; base += 32)
+        claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+      __syncwarp();
+      for (uint32_t i = lane; i < cap; i += 32) st_sm(wbase + 4 * i, 0u);
+    }
   }
   __syncwarp();
   st.fold();
@@ -630,14 +700,28 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
     const RankLayout L(span);
     for (uint32_t i = threadIdx.x; i < L.words(R.dl); i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
   } else if (R.dl <= kCtaHashDegMax) {
-    uint32_t lg = 32 - __clz(2 * R.dl - 1);
-    lg = max(5u, min(lg, kCtaWordsLg));
-    const uint32_t cap = 1u << lg;
-    for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
-    __syncthreads();
-    cta_claims<MODE, U>(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cap; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
+    const uint32_t blg = bucket_lg(R.dl);
+    bool done = false;
+    if (TL_BUCKET_PROBE && (4u << blg) <= kCtaWords) {
+      bool ok = true;
+      for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) ok &= bucket_insert(cbase, 32 - blg, __ldg(nl + i));
+      done = __syncthreads_and(ok) != 0;
+      if (done) cta_claims<MODE, U>(P, R, BucketProbe{cbase, 32 - blg}, lmax, a_orig, st);
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < (4u << blg); i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
+      __syncthreads();
+      if (!done && threadIdx.x == 0) *cta_cursor() = R.cb;  // the fallback restarts the record's claims
+    }
+    if (!done) {
+      uint32_t lg = 32 - __clz(2 * R.dl - 1);
+      lg = max(5u, min(lg, kCtaWordsLg));
+      const uint32_t cap = 1u << lg;
+      for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
+      __syncthreads();
+      cta_claims<MODE, U>(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < cap; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
+    }
   } else {
     __syncthreads();
     cta_claims<MODE, U>(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
@@ -665,7 +749,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
       const unsigned long long t = s_task;
       __syncthreads();
       if (t >= P.ncta) break;
-      cta_record<MODE, U>(P, P.crecs[t], cbase, st);
+      cta_record<MODE, U>(P, P.crecs[P.toff + t * P.tstride], cbase, st);
     }
   }
   // ---- phase 2: warp tasks
@@ -674,7 +758,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
     if (lane == 0) t = atomicAdd(P.acc + kWarpCounter, 1ull);
     t = __shfl_sync(kFull, t, 0);
     if (t >= P.ntasks) break;
-    const uint2 tk = P.tasks[P.ntasks - 1 - t];  // heaviest pivots (highest ranks) first
+    const uint2 tk = P.tasks[P.gtasks - 1 - (P.toff + t * P.tstride)];  // heaviest pivots (highest ranks) first
     for (uint32_t r = tk.x; r < tk.y; ++r) warp_record<MODE, U>(P, P.recs[r], wbase, st);
   }
   reduce_and_flush(st, P);
@@ -713,8 +797,10 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t 
   return lo;
 }
 
-// Cost-balanced cut of the claim index space: part p owns claims
-// [cut(p), cut(p+1)), cut(k) = first i with CP[i] + kKappa*i >= k*Total/nparts.
+// Cost cut of the claim index space: part p owns claims [cut(p), cut(p+1)),
+// cut(k) = first i with CP[i] + kKappa*i >= k*Total/nparts.  The parts'
+// logical-probe / table-build counters are attributed by this cut; the
+// execution is interleaved (aot_run) unless TL_SPLIT_MODE=range.
 // out: cb, ce, pb (pivot of cb), pe (one past the pivot of ce-1),
 //      vb, ve (pivot range attributed to this part), table_builds.
 __global__ void k_split(const uint64_t* CP, uint64_t m, const uint64_t* claim_off, const uint64_t* off, uint32_t n,
@@ -1107,7 +1193,23 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     }
   }
 
-  // adaptive task size: ~64 warp tasks per resident warp
+  // Multi-GPU execution: the cut above attributes the logical-probe and
+  // table-build counters (they only need to partition exactly); with
+  // interleaving (the default) every part then builds the whole graph's work
+  // records and runs every nparts-th task and CTA record, so each GPU gets an
+  // even mix of every probe path.  TL_SPLIT_MODE=range runs the cut's own
+  // claim range instead.
+  const uint64_t ccb = cb, cce = ce;
+  const uint32_t cpb = pb, cpe = pe;
+  const char* split_mode = getenv("TL_SPLIT_MODE");
+  const bool interleave = !whole && !(split_mode && std::string(split_mode) == "range");
+  if (interleave) {
+    cb = 0;
+    ce = m;
+    pb = 0;
+    pe = og.n;
+  }
+  // adaptive task size: ~64 warp tasks per resident warp (per part)
   uint64_t T = kTaskMin;
   bool long_lists = false;
   {
@@ -1122,7 +1224,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
       case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
       case AotMode::list: warps = resident_warps<AotMode::list>(); break;
     }
-    T = std::max<uint64_t>(kTaskMin, work / (uint64_t(std::max(warps, 1)) * 64));
+    T = std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
     long_lists = ce > cb && (w[1] - w[0]) / (ce - cb) >= TL_LONG_WINDOW;
   }
 
@@ -1210,9 +1312,12 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   P.out_cap = out_cap;
   P.recs = wrecs.p;
   P.tasks = tasks.p;
-  P.ntasks = G;
+  P.gtasks = G;
   P.crecs = crecs.p;
-  P.ncta = nc;
+  P.toff = interleave ? part : 0;
+  P.tstride = interleave ? nparts : 1;
+  P.ntasks = G > P.toff ? (G - P.toff + P.tstride - 1) / P.tstride : 0;
+  P.ncta = nc > P.toff ? (nc - P.toff + P.tstride - 1) / P.tstride : 0;
   switch (mode) {
     case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, long_lists, s); break;
     case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, long_lists, s); break;
@@ -1223,11 +1328,11 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     // edge index), a vertex share for the adaptive claims of cf-hash
     uint32_t vb = 0, ve = og.n;
     uint64_t eb = 0, ee = m;
-    if (fwd) {
-      vb = cb < ce ? pb : 0;
-      ve = cb < ce ? pe : 0;
-      eb = cb;
-      ee = ce;
+    if (fwd) {  // the counter cut's claims (= edges)
+      vb = ccb < cce ? cpb : 0;
+      ve = ccb < cce ? cpe : 0;
+      eb = ccb;
+      ee = cce;
     } else if (nparts > 1) {
       vb = uint32_t(uint64_t(og.n) * part / nparts);
       ve = uint32_t(uint64_t(og.n) * (part + 1) / nparts);
@@ -1255,7 +1360,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   r.hash_sum = h[kHsum];
   r.hash_xor = h[kHxor];
   r.emitted = h[kEmitted];
-  r.tasks = G + nc;
+  r.tasks = P.ntasks + P.ncta;
   r.triangles = r.positive + r.negative;
   switch (spec.algo) {  // the counters each kernel keeps (engine.hpp:164-276)
     case Algo::aot:

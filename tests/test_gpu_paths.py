@@ -1,11 +1,12 @@
-"""GPU: every probe path of k_aot (warp bitmap, warp rank bitmap, warp hash,
-CTA bitmap, CTA rank bitmap, CTA hash, global binary search) against the
-oracle.  The full configs reach the wide-window paths only at scale, so this
+"""GPU: every probe path of k_aot (warp bitmap, warp rank bitmap, warp hash --
+two-choice buckets, and the linear-probing fallback --, CTA bitmap, CTA rank
+bitmap, CTA hash, global binary search) against the oracle.  The full configs reach the wide-window paths only at scale, so this
 test runs tools/sanitize_run.py's parity workload (every kernel x mode x
 order, partitions, device verification) on a build of the library whose
 probe regions are shrunk (paper_2006_11494_b200/_build.py VARIANTS["paths"]),
-where small graphs exercise all of them, and checks from the path
-diagnostics (TL_DEBUG_PATHS) that each path carried work."""
+where small graphs exercise all of them (variants: rank bitmap on / off,
+bucket hashes forced to fail over to linear probing), and checks from the
+path diagnostics (TL_DEBUG_PATHS) that each path carried work."""
 import os
 import re
 import subprocess
@@ -23,7 +24,7 @@ def test_every_probe_path_matches_oracle(built):
     from paper_2006_11494_b200 import _build
 
     work = dict.fromkeys(PATHS, 0)
-    for variant in ("paths", "paths_hash"):  # the second disables the rank bitmap
+    for variant in ("paths", "paths_hash", "paths_fallback"):
         lib = _build.build_variant(variant)
         env = dict(os.environ, TL_LIB_PATH=lib, TL_DEBUG_PATHS="1")
         p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py"), "--size", "medium"],
