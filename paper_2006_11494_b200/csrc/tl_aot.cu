@@ -93,7 +93,7 @@ constexpr uint32_t kCtaWordsLg = 31 - __builtin_clz(kCtaWords);
 constexpr uint32_t kCtaHashDegMax = TL_CTA_HASH_DEG;  // larger pivots use the global binary search
 constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below this stay on the warp hash path
 #ifndef TL_EMIT_CAP
-#define TL_EMIT_CAP 96  // 4 CTAs/SM fit (128 hits: 3 CTAs, 32% slower at C4; tools/sweep.py)
+#define TL_EMIT_CAP 224  // hash mode staging (8-byte hits: 4 CTAs/SM fit; >= 32 x the long unroll; 192: +1%)
 #endif
 #ifndef TL_EMIT_CTAS
 #define TL_EMIT_CTAS 4
@@ -108,7 +108,7 @@ constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below thi
 #define TL_BUCKET_PROBE 1
 #endif
 #ifndef TL_LIST_CAP
-#define TL_LIST_CAP 96  // list mode (C2 4.9 ms vs 5.2 at 3 CTAs x 128, 6.2 at 4 x 64)
+#define TL_LIST_CAP 224  // list mode staging (hits per warp; >= 32 x the long unroll; 192: +1%)
 #endif
 #ifndef TL_LIST_CTAS
 #define TL_LIST_CTAS 4
@@ -383,12 +383,20 @@ __device__ __forceinline__ void hash_insert(uint32_t base, uint32_t mask, uint32
 }
 
 // ------------------------------------------------------------ emission
+// Hash / list modes stage hits per warp as 8-byte entries {neighbour id |
+// swap << 31, witness rank}; the pivot's original id is warp-uniform for a
+// whole record (`a_orig`), so a record's hits are flushed before the next
+// record starts.  Original ids are < 2^31 (n < 2^31), which frees bit 31 for
+// the cf-hash role swap of list mode (engine.hpp:212).
+constexpr uint32_t kSwapBit = 0x80000000u;
+
 template <AotMode MODE>
 struct Lane {
   uint32_t pos = 0, neg = 0;  // per record
   unsigned long long pos64 = 0, neg64 = 0, hsum = 0, hxor = 0;
   uint32_t ebase = 0;   // hash/list: byte address of the per-warp staging buffer
   uint32_t ecount = 0;  // warp-uniform
+  uint32_t a_orig = 0;  // the current record's pivot (original id)
   __device__ __forceinline__ void fold() {
     pos64 += pos;
     neg64 += neg;
@@ -396,9 +404,17 @@ struct Lane {
   }
 };
 
-// Hash / list modes stage hits per warp as (pivot id, neighbour id, witness
-// rank); a flush maps the witnesses to original ids with independent gathers
-// (all in flight at once) and then hashes or writes the whole batch.
+__device__ __forceinline__ void st_sm2(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
+__device__ __forceinline__ uint2 ld_sm2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
+// A flush maps the witnesses to original ids with independent gathers (all
+// in flight at once) and then hashes or writes the whole batch.
 template <AotMode MODE>
 __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
   if constexpr (MODE != AotMode::count) {
@@ -412,17 +428,19 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
       }
 #pragma unroll 4
       for (uint32_t i = lane_id(); i < cnt; i += 32) {
-        const uint32_t e = st.ebase + 12 * i;
-        uint32_t a = ld_sm(e), b = ld_sm(e + 4);
-        uint32_t c = __ldg(P.orig + ld_sm(e + 8));
+        const uint2 e = ld_sm2(st.ebase + 8 * i);
+        uint32_t c = __ldg(P.orig + e.y);
         if constexpr (MODE == AotMode::list) {
+          const uint32_t b = e.x & ~kSwapBit;
+          const bool sw = e.x & kSwapBit;
           if (base + i < P.out_cap) {
             uint32_t* o = P.out + 3 * (base + i);
-            o[0] = a;
-            o[1] = b;
+            o[0] = sw ? b : st.a_orig;
+            o[1] = sw ? st.a_orig : b;
             o[2] = c;
           }
         } else {
+          uint32_t a = st.a_orig, b = e.x;
           canon3(a, b, c);
           const uint64_t h = tri_hash(a, b, c);
           st.hsum += h;
@@ -435,32 +453,63 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
   }
 }
 
-// Warp-collective: every lane calls it once per probe round (hash/list
-// modes; counters are kept by the caller).  Emission role order (pivot,
-// neighbor, witness) as in engine.hpp:256 / :269.
+// Starts a record: the previous record's hits go out with its pivot.
 template <AotMode MODE>
-__device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, uint32_t a_orig, uint32_t b_orig,
-                                     uint32_t w) {
+__device__ __forceinline__ void begin_record(Lane<MODE>& st, const Params& P, uint32_t l) {
+  if constexpr (MODE != AotMode::count) {
+    const uint32_t a = __ldg(P.orig + l);
+    if (a != st.a_orig && st.ecount) flush_emits(st, P);
+    st.a_orig = a;
+  }
+}
+
+// Warp-collective: every lane calls it once per packed probe round (hash /
+// list modes; counters are kept by the caller).  `bw` = neighbour id | swap.
+template <AotMode MODE>
+__device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, uint32_t bw, uint32_t w) {
   const unsigned hm = __ballot_sync(kFull, hit);
   if (hm) {
     const uint32_t k = __popc(hm);
     if (st.ecount + k > emit_cap<MODE>()) flush_emits(st, P);
-    if (hit) {
-      const uint32_t slot = st.ebase + 12 * (st.ecount + __popc(hm & lanemask_lt()));
-      st_sm(slot, a_orig);
-      st_sm(slot + 4, b_orig);
-      st_sm(slot + 8, w);
-    }
+    if (hit) st_sm2(st.ebase + 8 * (st.ecount + __popc(hm & lanemask_lt())), bw, w);
     st.ecount += k;
   }
+}
+
+// Warp-collective: the hits of one group of U sweep rounds of one list (bit
+// k of `hm` = round k hit on this lane), all with the same neighbour word.
+template <AotMode MODE, int U>
+__device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint32_t hm, const uint32_t (&x)[U],
+                                           uint32_t bw) {
+  static_assert(32 * U <= emit_cap<MODE>(), "a group's hits must fit the staging buffer");
+  const uint32_t lane = lane_id();
+  const uint32_t c = __popc(hm);
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= uint32_t(o)) incl += t;
+  }
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  if (total == 0) return;
+  if (st.ecount + total > emit_cap<MODE>()) flush_emits(st, P);
+  uint32_t slot = st.ebase + 8 * (st.ecount + incl - c);
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    if ((hm >> k) & 1u) {
+      st_sm2(slot, bw, x[k]);
+      slot += 8;
+    }
+  }
+  st.ecount += total;
 }
 
 // ------------------------------------------------------------ claim batch
 // One warp processes claims [base, min(base + 32, ce)) of a pivot against the
 // staged probe side.  All 32 lanes must call it.
 template <AotMode MODE, int U, typename Probe>
-__device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe, uint32_t lmax, uint32_t a_orig,
-                                            uint64_t base, uint64_t ce, Lane<MODE>& st) {
+__device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe, uint32_t lmax, uint64_t base,
+                                            uint64_t ce, Lane<MODE>& st) {
   const uint32_t lane = lane_id();
   const uint64_t c = base + lane;
   uint64_t b = 0;
@@ -473,9 +522,9 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     len = (P.skip_neg && neg) ? 0u : uint32_t((w >> kWinLenShift) & kWinLenMask);
   }
   const uint32_t sflag = neg ? kNegBit : 0u;
-  uint32_t b_orig = 0;
+  uint32_t b_orig = 0;  // neighbour word: original id | swap (list-mode cf-hash negative claim)
   if constexpr (MODE != AotMode::count) {
-    if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit));
+    if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit)) | (MODE == AotMode::list && P.swap_neg && neg ? kSwapBit : 0u);
   }
 
   // ---- short claims: 32 probes per round, load-balanced over the lanes
@@ -514,10 +563,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     for (int k = 0; k < kSU; ++k) {
       const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
       if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
-      if constexpr (MODE != AotMode::count) {
-        const bool sw = MODE == AotMode::list && P.swap_neg && (of[k] & kNegBit);
-        emit(st, P, hit != 0, sw ? oo[k] : a_orig, sw ? a_orig : oo[k], x[k]);
-      }
+      if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, oo[k], x[k]);
     }
   }
 
@@ -531,14 +577,8 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     const uint64_t bj = __shfl_sync(kFull, b, j);
     const uint32_t lj = __shfl_sync(kFull, len, j);
     const bool nj = __shfl_sync(kFull, neg, j);
-    uint32_t oj = 0, ea = a_orig;
-    if constexpr (MODE != AotMode::count) {
-      oj = __shfl_sync(kFull, b_orig, j);
-      if (MODE == AotMode::list && P.swap_neg && nj) {
-        ea = oj;
-        oj = a_orig;
-      }
-    }
+    uint32_t oj = 0;
+    if constexpr (MODE != AotMode::count) oj = __shfl_sync(kFull, b_orig, j);
     const uint32_t* p = P.col + bj + lane;
     int rem = int(lj) - int(lane);  // this lane reads p[32k] while 32k < rem
     uint32_t hits = 0;
@@ -547,13 +587,15 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
 #pragma unroll
       for (int k = 0; k < U; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
       bool over = false;
+      uint32_t hm = 0;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         over |= x[k] > lmax;
         const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
         hits += hit;
-        if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, ea, oj, x[k]);
+        if constexpr (MODE != AotMode::count) hm |= hit << k;
       }
+      if constexpr (MODE != AotMode::count) emit_group<MODE, U>(st, P, hm, x, oj);
       p += 32 * U;
       rem -= 32 * U;
       if (__any_sync(kFull, over)) break;
@@ -588,13 +630,12 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
   const uint32_t* nl = P.col + R.lb;
   const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
   const uint32_t span = lmax - lmin + 1;
-  uint32_t a_orig = 0;
-  if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+  begin_record(st, P, R.l);
   if (span <= kWarpSpanMax) {
     for (uint32_t i = lane; i < R.dl; i += 32) bitmap_set(wbase, lmin, __ldg(nl + i));
     __syncwarp();
     const BitmapProbe probe{wbase, lmin, span};
-    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, base, R.ce, st);
     __syncwarp();
     const uint32_t nwords = (span + 31) >> 5;
     if (nwords <= max(64u, 2 * R.dl))
@@ -604,7 +645,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
   } else if (rank_fits(R.dl, span, kWarpWords)) {
     const RankProbe probe = rank_probe(wbase, lmin, span);
     const uint32_t nmask = rank_build(probe, nl, R.dl, span);
-    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+    for (uint64_t base = R.cb; base < R.ce; base += 32) claim_batch<MODE, U>(P, probe, lmax, base, R.ce, st);
     __syncwarp();
     const RankLayout L(span);
     for (uint32_t i = lane; i < L.nbw + L.ncw + nmask; i += 32) st_sm(wbase + 4 * i, 0u);
@@ -618,7 +659,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
       if (done) {
         const BucketProbe probe{wbase, 32 - blg};
         for (uint64_t base = R.cb; base < R.ce; base += 32)
-          claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+          claim_batch<MODE, U>(P, probe, lmax, base, R.ce, st);
       }
       __syncwarp();
       for (uint32_t i = lane; i < (4u << blg); i += 32) st_sm(wbase + 4 * i, 0u);
@@ -632,7 +673,7 @@ __device__ __forceinline__ void warp_record(const Params& P, const Rec& R, uint3
       __syncwarp();
       const HashProbe probe{wbase, cap - 1, 32 - lg};
       for (uint64_t base = R.cb; base < R.ce; base += 32)
-        claim_batch<MODE, U>(P, probe, lmax, a_orig, base, R.ce, st);
+        claim_batch<MODE, U>(P, probe, lmax, base, R.ce, st);
       __syncwarp();
       for (uint32_t i = lane; i < cap; i += 32) st_sm(wbase + 4 * i, 0u);
     }
@@ -655,7 +696,7 @@ __device__ unsigned long long* cta_cursor() {
 
 template <AotMode MODE, int U, typename Probe>
 __device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const Probe& probe, uint32_t lmax,
-                                           uint32_t a_orig, Lane<MODE>& st) {
+                                           Lane<MODE>& st) {
   unsigned long long* cur = cta_cursor();
   while (true) {
     // batches of 32 claims, then of TL_CTA_TAIL_BS once fewer than
@@ -669,7 +710,7 @@ __device__ __forceinline__ void cta_claims(const Params& P, const Rec& R, const 
     base = __shfl_sync(kFull, base, 0);
     bs = __shfl_sync(kFull, bs, 0);
     if (base >= R.ce) break;
-    claim_batch<MODE, U>(P, probe, lmax, a_orig, base, min(uint64_t(base + bs), R.ce), st);
+    claim_batch<MODE, U>(P, probe, lmax, base, min(uint64_t(base + bs), R.ce), st);
   }
 }
 
@@ -678,13 +719,12 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
   const uint32_t* nl = P.col + R.lb;
   const uint32_t lmin = __ldg(nl), lmax = __ldg(nl + R.dl - 1);
   const uint32_t span = lmax - lmin + 1;
-  uint32_t a_orig = 0;
-  if constexpr (MODE != AotMode::count) a_orig = __ldg(P.orig + R.l);
+  begin_record(st, P, R.l);
   if (threadIdx.x == 0) *cta_cursor() = R.cb;  // published by the barrier after the build
   if (span <= kCtaSpanMax) {
     for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) bitmap_set(cbase, lmin, __ldg(nl + i));
     __syncthreads();
-    cta_claims<MODE, U>(P, R, BitmapProbe{cbase, lmin, span}, lmax, a_orig, st);
+    cta_claims<MODE, U>(P, R, BitmapProbe{cbase, lmin, span}, lmax, st);
     __syncthreads();
     const uint32_t nwords = (span + 31) >> 5;
     if (nwords <= max(uint32_t(kWarpThreads), 2 * R.dl))
@@ -695,7 +735,7 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
     const RankProbe probe = rank_probe(cbase, lmin, span);
     if (threadIdx.x < 32) rank_build(probe, nl, R.dl, span);
     __syncthreads();
-    cta_claims<MODE, U>(P, R, probe, lmax, a_orig, st);
+    cta_claims<MODE, U>(P, R, probe, lmax, st);
     __syncthreads();
     const RankLayout L(span);
     for (uint32_t i = threadIdx.x; i < L.words(R.dl); i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
@@ -706,7 +746,7 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
       bool ok = true;
       for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) ok &= bucket_insert(cbase, 32 - blg, __ldg(nl + i));
       done = __syncthreads_and(ok) != 0;
-      if (done) cta_claims<MODE, U>(P, R, BucketProbe{cbase, 32 - blg}, lmax, a_orig, st);
+      if (done) cta_claims<MODE, U>(P, R, BucketProbe{cbase, 32 - blg}, lmax, st);
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < (4u << blg); i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
       __syncthreads();
@@ -718,13 +758,13 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
       const uint32_t cap = 1u << lg;
       for (uint32_t i = threadIdx.x; i < R.dl; i += kWarpThreads) hash_insert(cbase, cap - 1, 32 - lg, __ldg(nl + i));
       __syncthreads();
-      cta_claims<MODE, U>(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, a_orig, st);
+      cta_claims<MODE, U>(P, R, HashProbe{cbase, cap - 1, 32 - lg}, lmax, st);
       __syncthreads();
       for (uint32_t i = threadIdx.x; i < cap; i += kWarpThreads) st_sm(cbase + 4 * i, 0u);
     }
   } else {
     __syncthreads();
-    cta_claims<MODE, U>(P, R, GlobalProbe{nl, R.dl}, lmax, a_orig, st);
+    cta_claims<MODE, U>(P, R, GlobalProbe{nl, R.dl}, lmax, st);
   }
   st.fold();
 }
@@ -738,7 +778,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
   Lane<MODE> st;
-  st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (3 * emit_cap<MODE>()));
+  st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (2 * emit_cap<MODE>()));
   __syncthreads();
   // ---- phase 1: CTA records
   if (P.ncta) {
@@ -1036,7 +1076,7 @@ int sm_count() {
 
 template <AotMode MODE>
 size_t kernel_smem() {
-  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 3 * emit_cap<MODE>() : 0));
+  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0));
 }
 
 template <AotMode MODE>

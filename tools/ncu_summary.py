@@ -87,7 +87,7 @@ def top_lines(report, n=12):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
-    ap.add_argument("launch_csv")
+    ap.add_argument("launch_csv", nargs="?")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic")
@@ -96,11 +96,13 @@ def main():
     d = details(a.report)
     rw = raw(a.report)
     kname = next(iter(v[2] for v in d.values() if v[2]), "?")
-    dram_r = num(rw.get("dram__bytes_read.sum", ("", 0))[1])
-    dram_w = num(rw.get("dram__bytes_write.sum", ("", 0))[1])
-    unit_r = rw.get("dram__bytes_read.sum", ("byte", 0))[0]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-    traffic = (dram_r + dram_w) * scale
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+    def nbytes(metric):  # each metric carries its own unit
+        unit, v = rw.get(metric, ("byte", 0))
+        return num(v) * scale.get(unit, 1)
+
+    traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
     keys = ["Duration", "Elapsed Cycles", "SM Active Cycles", "Executed Ipc Active", "Issue Slots Busy",
             "Issued Instructions", "Registers Per Thread", "Theoretical Occupancy", "Achieved Occupancy",
             "L1/TEX Hit Rate", "L2 Hit Rate", "L1/TEX Cache Throughput", "L2 Cache Throughput", "DRAM Throughput",
@@ -112,11 +114,11 @@ def main():
         if k in d:
             lines.append(f"| {k} | {d[k][0]} {d[k][1]} |")
     lines.append(f"| dram__bytes_read.sum + dram__bytes_write.sum | {traffic / 1e9:.3f} GB per launch |")
-    agg = launches(a.launch_csv)
+    agg = launches(a.launch_csv) if a.launch_csv else {}
     tot = sum(t for _, t in agg.values()) or 1
-    lines += ["", "## launch list (cold-cache, serialised: compare shares)", "",
+    lines += [] if not agg else ["", "## launch list (cold-cache, serialised: compare shares)", "",
               "| kernel | launches | avg µs | share of listed GPU time |", "|---|---|---|---|"]
-    for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:16]:
+    for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:16]:  # noqa: B007
         lines.append(f"| `{name[:70]}` | {c} | {t / c:.1f} | {100 * t / tot:.1f}% |")
     lines += ["", "## top source lines by stall samples", "", "| line | stall % | inst % | top stalls | source |",
               "|---|---|---|---|---|"]
