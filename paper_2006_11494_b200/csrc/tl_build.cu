@@ -9,6 +9,7 @@
 // the bits the keys actually use (2 * ceil(log2 n) for packed vertex pairs).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -265,6 +266,67 @@ __global__ void k_windows(uint64_t* val_win, uint64_t m, const uint64_t* off, ui
 }
 
 // ------------------------------------------------ reference-layout transfer
+// Rows [u0, u1) of the reference layout straight to rank-space col + claims
+// + cost model (k_rows_to_keys, k_low_bits and k_claims in one pass), valid
+// when every row is rank-ascending (flags bit0 clear; else the caller falls
+// back to the sorting path).  Eight lanes per row.  orig[t] = u and orig[h] =
+// v, so the (deg+, id) tie-break needs no gather.
+__global__ void k_rows_claims(const uint64_t* out_off, const uint32_t* out, const uint32_t* rank, uint32_t n,
+                              uint32_t u0, uint32_t u1, const uint64_t* off, uint32_t* col, uint32_t* ckey,
+                              uint64_t* val, unsigned long long* costs, uint32_t* max_out, uint32_t* flags) {
+  constexpr uint32_t G = 8;
+  const uint32_t gl = threadIdx.x & (G - 1);
+  const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+  const uint64_t groups = (uint64_t(gridDim.x) * blockDim.x) / G;
+  unsigned long long cf = 0, kc = 0, ao = 0;
+  uint32_t mx = 0, f = 0;
+  for (uint64_t u = u0 + (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G; u < u1; u += groups) {
+    const uint32_t t = rank[u];
+    const uint64_t src = out_off[u], len = out_off[u + 1] - src, dst = off[t];
+    const uint32_t dt = uint32_t(len);
+    mx = max(mx, dt);
+    uint32_t carry = t;
+    for (uint64_t j0 = 0; j0 < len; j0 += G) {
+      const uint64_t j = j0 + gl;
+      const bool valid = j < len;
+      uint32_t h = 0;
+      if (valid) {
+        const uint32_t v = out[src + j];
+        h = v < n ? rank[v] : 0;
+        if (v >= n || h <= t) f |= 2u;
+        const uint32_t dh = v < n ? uint32_t(off[h + 1] - off[h]) : 0u;
+        cf += dt + dh;  // engine.cpp:43-45
+        kc += dh;
+        ao += min(dt, dh);
+        const bool h_first = dh != dt ? dh < dt : v < uint32_t(u);
+        col[dst + j] = h;
+        ckey[dst + j] = h_first ? t : h;
+        val[dst + j] = h_first ? uint64_t(h) : ((uint64_t(j + 1) << 32) | t | kNegBit);
+      }
+      uint32_t prev = __shfl_up_sync(gmask, h, 1, G);
+      if (gl == 0) prev = carry;
+      if (valid && h <= prev) f |= 1u;
+      const uint32_t last = uint32_t(len - j0 < G ? len - j0 - 1 : G - 1);
+      carry = __shfl_sync(gmask, h, last, G);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    cf += __shfl_xor_sync(0xFFFFFFFFu, cf, o);
+    kc += __shfl_xor_sync(0xFFFFFFFFu, kc, o);
+    ao += __shfl_xor_sync(0xFFFFFFFFu, ao, o);
+    mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    f |= __shfl_xor_sync(0xFFFFFFFFu, f, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (cf) atomicAdd(costs + 0, cf);
+    if (kc) atomicAdd(costs + 1, kc);
+    if (ao) atomicAdd(costs + 2, ao);
+    if (mx) atomicMax(max_out, mx);
+    if (f) atomicOr(flags, f);
+  }
+}
+
+
 __global__ void k_rank_degrees(const uint32_t* orig, uint32_t n, const uint64_t* out_off, uint64_t* deg) {
   TL_GRID_STRIDE(r, uint64_t(n) + 1) {
     if (r < n) {
@@ -605,10 +667,13 @@ bool is_permutation(const uint32_t* d_rank, uint32_t n, cudaStream_t s) {
 
 namespace {
 
+void finish_claims(tl_oriented& og, DBuf<uint32_t>& ckey, DBuf<uint64_t>& dk, DBuf<uint64_t>& scal);
+
 // Shared tail of orient / oriented_from_csr: `dk` holds the m rank-sorted
 // directed keys (t << nb | h) and og.off/og.orig/og.rank are set.
 void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   cudaStream_t s = og.stream;
+  const PhaseClock clk("finish", s);
   const uint64_t m = og.m;
   og.col.alloc(std::max<uint64_t>(m, 1), s);
   og.claim_off.alloc(uint64_t(og.n) + 1, s);
@@ -625,15 +690,26 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   }
   k_low_bits<<<grid_for(m, kBlock, 148u * 64u), kBlock, 0, s>>>(dk.p, m, og.nb, og.col.p);
   TL_CUDA(cudaGetLastError());
-  DBuf<uint32_t> ckey, ckey2;
+  DBuf<uint32_t> ckey;
   ckey.alloc(m, s);
   k_claims<<<grid_for(m, kBlock, 148u * 64u), kBlock, 0, s>>>(
       dk.p, ckey.p, m, og.nb, og.off.p, og.orig.p, reinterpret_cast<unsigned long long*>(scal.p),
       reinterpret_cast<uint32_t*>(scal.p + 3));
   TL_CUDA(cudaGetLastError());
+  clk.mark("low_bits+claims");
+  finish_claims(og, ckey, dk, scal);
+}
+
+// Claims (ckey = pivot, val = pos << 32 | s | neg << 31, in rank-sorted edge
+// order) -> grouped by pivot, windows; scal = {cf, kclist, aot, max deg+}.
+void finish_claims(tl_oriented& og, DBuf<uint32_t>& ckey, DBuf<uint64_t>& dk, DBuf<uint64_t>& scal) {
+  cudaStream_t s = og.stream;
+  const PhaseClock clk("claims", s);
+  const uint64_t m = og.m;
   uint64_t host[4];
   TL_CUDA(cudaMemcpyAsync(host, scal.p, 32, cudaMemcpyDeviceToHost, s));
   // group claims by pivot (stable: deterministic order inside a pivot)
+  DBuf<uint32_t> ckey2;
   ckey2.alloc(m, s);
   DBuf<uint64_t> val2;
   val2.alloc(m, s);
@@ -642,6 +718,7 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   val2.reset();
   fill_offsets(ckey.p, 0, m, og.n, og.claim_off.p, s);
   TL_CUDA(cudaStreamSynchronize(s));
+  clk.mark("claim_sort");
   og.cost[0] = host[0];
   og.cost[1] = host[1];
   og.cost[2] = host[2];
@@ -654,6 +731,7 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   og.win = std::move(dk);
   og.claim_s = std::move(ckey);
   TL_CUDA(cudaStreamSynchronize(s));
+  clk.mark("windows");
 }
 
 }  // namespace
@@ -691,6 +769,7 @@ void orient(tl_graph& g, const uint32_t* d_rank, tl_oriented& og) {
 void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* d_out_off, const uint32_t* d_out,
                        const uint32_t* d_rank) {
   cudaStream_t s = og.stream;
+  const PhaseClock clk("from_csr", s);
   TL_REQUIRE(n < (1u << 31), TL_EINVAL, "the B200 path supports fewer than 2^31 vertices");
   og.n = n;
   og.nb = std::max<uint32_t>(1, bits_for(n));
@@ -726,6 +805,7 @@ void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* 
     TL_CUDA(cudaGetLastError());
   }
   uint32_t f = d2h_scalar(flags.p, s);
+  clk.mark("rows_to_keys");
   TL_REQUIRE(!(f & 2u), TL_EINVAL, "out-lists contain an edge that does not point to higher rank");
   if (f & 1u) {  // a local order other than rank-asc: restore rank-ascending lists
     DBuf<uint64_t> tmp;
@@ -733,6 +813,123 @@ void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* 
     radix_sort_keys(dk, tmp, m, int(2 * og.nb), s);
   }
   finish_orient(og, dk);
+}
+
+// Upload of a host OrientedGraph in the reference layout with the transfer
+// of the out-lists overlapped: rows are cut into chunks of about equal edge
+// counts on the host offsets, each chunk is copied on a copy stream and, as
+// soon as it lands, converted on the graph stream straight to rank-space col
+// + claims (k_rows_claims).  Lists that are not rank-ascending (another local
+// order) take the sorting path over the resident copy.
+void oriented_from_host_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* h_off, const uint32_t* h_out,
+                            const uint32_t* h_rank) {
+  cudaStream_t s = og.stream;
+  const PhaseClock clk("from_host_csr", s);
+  TL_REQUIRE(n < (1u << 31), TL_EINVAL, "the B200 path supports fewer than 2^31 vertices");
+  TL_REQUIRE(h_off[n] == m, TL_EINVAL, "out_offsets[n] does not equal m");
+  og.n = n;
+  og.nb = std::max<uint32_t>(1, bits_for(n));
+  og.m = m;
+  DBuf<uint64_t> d_off;
+  DBuf<uint32_t> d_out, d_rank;
+  d_off.alloc(uint64_t(n) + 1, s);
+  d_out.alloc(std::max<uint64_t>(m, 1), s);
+  d_rank.alloc(std::max<uint64_t>(n, 1), s);
+  if (n) TL_CUDA(cudaMemcpyAsync(d_rank.p, h_rank, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+  TL_CUDA(cudaMemcpyAsync(d_off.p, h_off, sizeof(uint64_t) * (uint64_t(n) + 1), cudaMemcpyHostToDevice, s));
+  // chunk c = rows [cut[c], cut[c+1]), about m / nchunks edges each
+  uint32_t nchunks = uint32_t(std::min<uint64_t>(16, std::max<uint64_t>(1, m >> 26)));
+  if (const char* e = getenv("TL_UPLOAD_CHUNKS")) nchunks = uint32_t(std::max(1, std::min(64, atoi(e))));  // tests
+  std::vector<uint32_t> cut(nchunks + 1, n);
+  cut[0] = 0;
+  for (uint32_t c = 1; c < nchunks; ++c)
+    cut[c] = uint32_t(std::lower_bound(h_off, h_off + n + 1, m * c / nchunks) - h_off);
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ev(nchunks + 1, nullptr);
+  auto release = [&] {
+    if (cs) cudaStreamSynchronize(cs);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+    cs = nullptr;
+    for (auto& e : ev) e = nullptr;
+  };
+  DBuf<uint32_t> ckey, flags;
+  DBuf<uint64_t> val, scal;
+  uint32_t f = 0;
+  try {
+    TL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (auto& e : ev) TL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(ev[nchunks], s));  // the allocations above are stream-ordered on s
+    TL_CUDA(cudaStreamWaitEvent(cs, ev[nchunks], 0));
+    for (uint32_t c = 0; c < nchunks && m; ++c) {
+      const uint64_t b = h_off[cut[c]], e = h_off[cut[c + 1]];
+      if (e > b) TL_CUDA(cudaMemcpyAsync(d_out.p + b, h_out + b, sizeof(uint32_t) * (e - b), cudaMemcpyHostToDevice, cs));
+      TL_CUDA(cudaEventRecord(ev[c], cs));
+    }
+    TL_REQUIRE(is_permutation(d_rank.p, n, s), TL_EINVAL, "order is not a permutation of the vertex set");
+    og.rank = std::move(d_rank);
+    og.orig.alloc(std::max<uint64_t>(n, 1), s);
+    og.off.alloc(uint64_t(n) + 1, s);
+    if (n) k_invert<<<grid_for(n, kBlock), kBlock, 0, s>>>(og.rank.p, n, og.orig.p);
+    {
+      DBuf<uint64_t> deg;
+      deg.alloc(uint64_t(n) + 1, s);
+      k_rank_degrees<<<grid_for(uint64_t(n) + 1, kBlock), kBlock, 0, s>>>(og.orig.p, n, d_off.p, deg.p);
+      TL_CUDA(cudaGetLastError());
+      cub_call(s, [&](void* t, size_t& bytes) {
+        return cub::DeviceScan::ExclusiveSum(t, bytes, deg.p, og.off.p, uint64_t(n) + 1, s);
+      });
+    }
+    clk.mark("offsets");
+    og.col.alloc(std::max<uint64_t>(m, 1), s);
+    ckey.alloc(std::max<uint64_t>(m, 1), s);
+    val.alloc(std::max<uint64_t>(m, 1), s);
+    scal.alloc(4, s);
+    flags.alloc(1, s);
+    TL_CUDA(cudaMemsetAsync(scal.p, 0, 32, s));
+    TL_CUDA(cudaMemsetAsync(flags.p, 0, 4, s));
+    for (uint32_t c = 0; c < nchunks && m; ++c) {
+      TL_CUDA(cudaStreamWaitEvent(s, ev[c], 0));
+      const uint64_t rows = cut[c + 1] - cut[c];
+      if (!rows) continue;
+      k_rows_claims<<<grid_for(rows * 8, kBlock, 148u * 64u), kBlock, 0, s>>>(
+          d_off.p, d_out.p, og.rank.p, n, cut[c], cut[c + 1], og.off.p, og.col.p, ckey.p, val.p,
+          reinterpret_cast<unsigned long long*>(scal.p), reinterpret_cast<uint32_t*>(scal.p + 3), flags.p);
+      TL_CUDA(cudaGetLastError());
+    }
+    f = d2h_scalar(flags.p, s);
+    clk.mark("rows_claims");
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+  TL_REQUIRE(!(f & 2u), TL_EINVAL, "out-lists contain an edge that does not point to higher rank");
+  if (m == 0 || (f & 1u)) {  // empty, or a local order other than rank-asc: restore rank-ascending lists
+    og.col.reset();
+    ckey.reset();
+    val.reset();
+    DBuf<uint64_t> dk;
+    dk.alloc(std::max<uint64_t>(m, 1), s);
+    TL_CUDA(cudaMemsetAsync(flags.p, 0, 4, s));
+    if (m) {
+      k_rows_to_keys<<<grid_for(uint64_t(n) * 8, kBlock, 148u * 64u), kBlock, 0, s>>>(
+          d_off.p, d_out.p, og.rank.p, n, og.nb, og.off.p, dk.p, flags.p);
+      TL_CUDA(cudaGetLastError());
+      DBuf<uint64_t> tmp;
+      tmp.alloc(m, s);
+      radix_sort_keys(dk, tmp, m, int(2 * og.nb), s);
+    }
+    d_out.reset();
+    d_off.reset();
+    finish_orient(og, dk);
+    return;
+  }
+  d_out.reset();
+  d_off.reset();
+  og.claim_off.alloc(uint64_t(n) + 1, s);
+  finish_claims(og, ckey, val, scal);
 }
 
 // Reference OrientedGraph layout (original ids): out_offsets/out by id, in

@@ -368,15 +368,7 @@ int tl_oriented_from_csr(uint32_t n, uint64_t m, const uint64_t* out_offsets, co
       TL_CUDA(cudaStreamWaitEvent(s, ev, 0));
       cudaEventDestroy(ev);
     }
-    tlb::DBuf<uint64_t> d_off;
-    tlb::DBuf<uint32_t> d_out, d_rank;
-    d_off.alloc(uint64_t(n) + 1, s);
-    d_out.alloc(std::max<uint64_t>(m, 1), s);
-    d_rank.alloc(std::max<uint64_t>(n, 1), s);
-    TL_CUDA(cudaMemcpyAsync(d_off.p, out_offsets, sizeof(uint64_t) * (uint64_t(n) + 1), cudaMemcpyHostToDevice, s));
-    if (m) TL_CUDA(cudaMemcpyAsync(d_out.p, out, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, s));
-    if (n) TL_CUDA(cudaMemcpyAsync(d_rank.p, rank, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
-    tlb::oriented_from_csr(*og, n, m, d_off.p, d_out.p, d_rank.p);
+    tlb::oriented_from_host_csr(*og, n, m, out_offsets, out, rank);
     TL_CUDA(cudaStreamSynchronize(s));
     *out_graph = og.release();
   });

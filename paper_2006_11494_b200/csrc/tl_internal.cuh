@@ -1,6 +1,9 @@
 // tl_internal.cuh -- device-resident graph handles and pipeline entry points.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 
@@ -76,6 +79,22 @@ struct DeviceGuard {
   }
 };
 
+// TL_DEBUG_PREP=1: host-side phase timeline (synchronises the stream at
+// every mark, so only for diagnosis).
+struct PhaseClock {
+  const char* tag;
+  cudaStream_t s;
+  bool on = getenv("TL_DEBUG_PREP") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  PhaseClock(const char* tag_, cudaStream_t s_) : tag(tag_), s(s_) {}
+  void mark(const char* what) const {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[tl %s] %-14s %9.3f ms\n", tag, what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 // ---- tl_build.cu ----
 void gen_er(uint64_t seed, uint32_t n, uint64_t npairs, uint32_t* d_pairs, cudaStream_t s);
 void gen_rmat(uint64_t seed, uint32_t scale, uint64_t npairs, uint32_t* d_pairs, cudaStream_t s);
@@ -98,6 +117,8 @@ void degree_order(tl_graph& g, DBuf<uint32_t>& rank);  // device rank[n]
 void orient(tl_graph& g, const uint32_t* d_rank, tl_oriented& og);
 void oriented_from_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* d_out_off,
                        const uint32_t* d_out, const uint32_t* d_rank);
+void oriented_from_host_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint64_t* h_off, const uint32_t* h_out,
+                            const uint32_t* h_rank);
 void oriented_download(tl_oriented& og, uint64_t* out_off, uint32_t* out, uint64_t* in_off,
                        uint32_t* in, uint32_t* rank);
 bool is_permutation(const uint32_t* d_rank, uint32_t n, cudaStream_t s);

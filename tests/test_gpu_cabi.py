@@ -235,6 +235,51 @@ def test_upload_reference_layout_matches_orient():
     assert upd.hash()["hash_sum"] == want["hash_sum"]
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+def test_upload_chunked_transfer(monkeypatch, chunks):
+    """The overlapped upload (out-lists copied in row chunks and converted as
+    they land) gives the same oriented graph for any chunking, including
+    chunks of zero rows, and with a degree-desc local order (sorting path)."""
+    monkeypatch.setenv("TL_UPLOAD_CHUNKS", str(chunks))
+    pairs = O.gen_rmat(9, 11, 12 << 11)
+    for local in ("rank-asc", "degree-desc"):
+        ref = O.RefGraph(1 << 11, pairs, local=local)
+        a = ref.oriented_csr()
+        up = capi.DeviceOriented.from_csr(ref.n, a["out_offsets"], a["out"], a["rank"])
+        want = ref.hash(threads=2)
+        got = up.hash()
+        for k in ("triangles", "probes", "positive_triangles", "negative_triangles", "hash_sum", "hash_xor"):
+            assert got[k] == want[k], (local, k)
+        assert up.cost_model() == ref.cost_model()
+        assert up.max_out_degree == ref.max_out_degree()
+        if local == "rank-asc":
+            b = up.csr()
+            for k in ("out_offsets", "out", "in_offsets", "inn", "rank"):
+                assert np.array_equal(a[k], b[k]), k
+    tiny = O.RefGraph(3, O.as_pairs([]))  # m = 0
+    t = tiny.oriented_csr()
+    assert capi.DeviceOriented.from_csr(3, t["out_offsets"], t["out"], t["rank"]).count()["triangles"] == 0
+
+
+def test_upload_rejects_bad_layouts():
+    """ordering.cpp:187-188 (not a permutation), a wrong out_offsets[n], and an
+    edge against the order are TL_EINVAL, with the copy stream drained."""
+    pairs = O.gen_rmat(4, 9, 8 << 9)
+    ref = O.RefGraph(1 << 9, pairs)
+    a = ref.oriented_csr()
+    bad_rank = a["rank"].copy()
+    bad_rank[0] = bad_rank[1]
+    bad_off = a["out_offsets"].copy()
+    bad_off[-1] += 1
+    flipped = a["rank"].max() - a["rank"]  # every edge now points to lower rank
+    for off, rank in ((a["out_offsets"], bad_rank), (bad_off, a["rank"]), (a["out_offsets"], flipped)):
+        with pytest.raises(capi.TlError) as e:
+            capi.DeviceOriented.from_csr(ref.n, off, a["out"], rank.astype(np.uint32))
+        assert e.value.code == capi.TL_EINVAL
+    ok = capi.DeviceOriented.from_csr(ref.n, a["out_offsets"], a["out"], a["rank"])  # the device is still usable
+    assert ok.count()["triangles"] == ref.count()["triangles"]
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("key", ["c2", "c3", "c4"])
 def test_config_vs_reference(golden, key):
