@@ -273,10 +273,18 @@ def run_ours(args):
     from paper_2006_11494_b200.configs import CONFIGS
 
     rank, world, local = dist_env()
+    # TL_BENCH_BACKEND=gloo: functional check of the N>1 path with fewer GPUs
+    # than ranks (ranks share a device; their kernels never wait on each
+    # other, the collectives run on the host) -- not a measurement
+    backend = os.environ.get("TL_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = CONFIGS[args.config]
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream

@@ -1275,11 +1275,17 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     TL_CUDA(cudaMemcpyAsync(w + 1, CP.p + ce, 8, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaStreamSynchronize(s));
     const uint64_t work = (w[1] - w[0]) + kKappa * (ce - cb);
-    int warps = 0;
-    switch (mode) {
-      case AotMode::count: warps = resident_warps<AotMode::count>(); break;
-      case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
-      case AotMode::list: warps = resident_warps<AotMode::list>(); break;
+    // A part's work must not depend on the mode: listing sizes its buffer by
+    // a counting pass over the same part (and the ranks of one job may run
+    // different modes), so a partitioned run sizes tasks for the count
+    // kernel's residency in every mode.
+    int warps = resident_warps<AotMode::count>();
+    if (nparts == 1) {
+      switch (mode) {
+        case AotMode::count: break;
+        case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
+        case AotMode::list: warps = resident_warps<AotMode::list>(); break;
+      }
     }
     T = std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
     long_lists = ce > cb && (w[1] - w[0]) / (ce - cb) >= TL_LONG_WINDOW;

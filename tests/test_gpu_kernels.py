@@ -197,3 +197,33 @@ def test_full_config_every_kernel_vs_reference_golden(key):
             assert all(got[k] == want[k] for k in COUNTERS), (key, order, name, got, want)
             assert (got["hash_sum"], got["hash_xor"]) == (want["hash_sum"], want["hash_xor"]), (key, order, name)
         og.close()
+
+
+def test_partitioned_listing_at_scale():
+    """The multi-GPU cut at a size where the task size exceeds its floor
+    (C3, 4 parts): every part's listing (buffer sized by a counting pass over
+    the same part) succeeds and emits exactly its counted triangles, and the
+    parts add up to the reference's total (tests/golden/configs.json)."""
+    import torch
+
+    cfg = CONFIGS["c3"]
+    d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
+    capi.gen_pairs_device(cfg, d.data_ptr())
+    g = capi.DeviceGraph.from_device_pairs(d.data_ptr(), cfg["npairs"], cfg["n"])
+    del d
+    og = g.orient()
+    g.close()
+    torch.cuda.empty_cache()
+    total, nparts = 0, 4
+    for p in range(nparts):
+        counted = og.count(part=p, nparts=nparts)["triangles"]
+        s = capi.TlStats()
+        o = capi.run_options(False, p, nparts)
+        capi._check(capi.lib().tl_aot_list(og._h, capi.C.byref(o), None, 0, 0, capi.C.byref(s)))
+        listed = s.as_dict()
+        assert listed["triangles"] == counted, p
+        assert og.hash(part=p, nparts=nparts)["triangles"] == counted, p
+        total += counted
+    golden = json.load(open(os.path.join(os.path.dirname(GOLDEN), "configs.json")))["c3"]
+    assert total == golden["triangles"]
+    og.close()
