@@ -114,6 +114,15 @@ def main():
         if k in d:
             lines.append(f"| {k} | {d[k][0]} {d[k][1]} |")
     lines.append(f"| dram__bytes_read.sum + dram__bytes_write.sum | {traffic / 1e9:.3f} GB per launch |")
+    for key, label in (("lts__t_sector_hit_rate.pct", "L2 sector hit rate (lts__t_sector_hit_rate.pct)"),
+                       ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                        "shared-memory wavefronts, % of peak"),
+                       ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "shared-memory load bank conflicts"),
+                       ("memory_l1_wavefronts_shared", "shared-memory wavefronts (actual)"),
+                       ("memory_l1_wavefronts_shared_ideal", "shared-memory wavefronts (conflict-free ideal)")):
+        if key in rw:
+            unit, v = rw[key]
+            lines.append(f"| {label} | {v} {unit} |")
     agg = launches(a.launch_csv) if a.launch_csv else {}
     tot = sum(t for _, t in agg.values()) or 1
     lines += [] if not agg else ["", "## launch list (cold-cache, serialised: compare shares)", "",
