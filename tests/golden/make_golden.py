@@ -77,6 +77,8 @@ def golden_for(key: str, threads: int) -> dict:
 def main(keys):
     threads = O.hardware_threads()
     path = os.path.join(HERE, "configs.json")
+    if keys and keys[0] == "--out":  # e.g. on a GPU box's host for C5: write elsewhere, merge here
+        path, keys = keys[1], keys[2:]
     data = json.load(open(path)) if os.path.exists(path) else {}
     for k in keys:
         t = time.time()
