@@ -30,10 +30,26 @@ from paper_2006_11494_b200.configs import CONFIGS  # noqa: E402
 from oracle import pairs_checksum  # noqa: E402
 
 
-def golden_for(key: str, threads: int) -> dict:
+def device_pairs(cfg: dict) -> np.ndarray:
+    """The same pair list from the device generator (bit-identical to the C
+    restatement's: full checksums agree on C1-C4, tests/test_gpu_cabi.py) --
+    minutes faster at C5, where the reference then runs on a GPU box's host."""
+    import torch
+
+    from paper_2006_11494_b200 import capi
+
+    d = torch.empty(2 * cfg["npairs"], dtype=torch.int32, device="cuda")
+    capi.gen_pairs_device(cfg, d.data_ptr())
+    host = d.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    del d
+    torch.cuda.empty_cache()
+    return host
+
+
+def golden_for(key: str, threads: int, on_device: bool = False) -> dict:
     cfg = CONFIGS[key]
     t0 = time.time()
-    pairs = O.gen_config(cfg)
+    pairs = device_pairs(cfg) if on_device else O.gen_config(cfg)
     t_gen = time.time() - t0
     checksum, first = pairs_checksum(pairs), pairs[:8].tolist()
     npairs = int(pairs.shape[0])
@@ -63,6 +79,7 @@ def golden_for(key: str, threads: int) -> dict:
         "ref_list_wall_s": h["wall_time_s"],
         "ref_threads": threads,
         "gen_s": t_gen,
+        "pairs_from": "device generator" if on_device else "C restatement generator",
     }
     if key == "c1":
         st, raw = ref.collect(threads=threads)
@@ -77,12 +94,15 @@ def golden_for(key: str, threads: int) -> dict:
 def main(keys):
     threads = O.hardware_threads()
     path = os.path.join(HERE, "configs.json")
+    on_device = False
     if keys and keys[0] == "--out":  # e.g. on a GPU box's host for C5: write elsewhere, merge here
         path, keys = keys[1], keys[2:]
+    if keys and keys[0] == "--device-pairs":
+        on_device, keys = True, keys[1:]
     data = json.load(open(path)) if os.path.exists(path) else {}
     for k in keys:
         t = time.time()
-        data[k] = golden_for(k, threads)
+        data[k] = golden_for(k, threads, on_device)
         print(k, {x: data[k][x] for x in ("m", "triangles", "hash_sum")}, f"{time.time() - t:.1f}s", flush=True)
         json.dump(data, open(path, "w"), indent=1, sort_keys=True)
 

@@ -318,13 +318,16 @@ def test_config_vs_reference(golden, key):
 
 
 @pytest.mark.slow
-def test_c5_rmat28_self_consistency():
+def test_c5_rmat28_self_consistency(golden):
     """C5 (R-MAT s28, 4.29e9 pairs) fits one B200.  The reference cannot run it
-    in the build container (> 100 GB host memory), so it is checked through
-    size-independent identities: probes == aot_cost (cost model accumulated in
-    a separate pass), positive + negative == triangles, the hash mode counts
-    the same triangles, and two cost-balanced parts sum/xor to the whole --
-    the multi-GPU decomposition on one device."""
+    in the build container (> 100 GB host memory); it ran once on a GPU box's
+    host (tests/golden/make_golden.py --device-pairs c5) and, where that golden
+    entry exists, every counter, the cost model and the triangle hash are
+    compared with it.  Size-independent identities are checked as well:
+    probes == aot_cost (cost model accumulated in a separate pass), positive +
+    negative == triangles, the hash mode counts the same triangles, and two
+    cost-balanced parts sum/xor to the whole -- the multi-GPU decomposition
+    on one device."""
     import torch
 
     cfg = CONFIGS["c5"]
@@ -350,3 +353,10 @@ def test_c5_rmat28_self_consistency():
     assert sum(p["table_builds"] for p in parts) == do.m
     assert (parts[0]["hash_sum"] + parts[1]["hash_sum"]) % (1 << 64) == h["hash_sum"]
     assert parts[0]["hash_xor"] ^ parts[1]["hash_xor"] == h["hash_xor"]
+    if "c5" in golden:
+        g = golden["c5"]
+        assert (do.n, do.m, do.max_out_degree) == (g["n"], g["m"], g["max_out_degree"])
+        assert cm == g["cost_model"]
+        for k in ("triangles", "probes", "table_builds", "positive_triangles", "negative_triangles", "hash_sum",
+                  "hash_xor"):
+            assert h[k] == g[k], k
