@@ -118,6 +118,12 @@ template <AotMode MODE>
 constexpr int emit_cap() {
   return MODE == AotMode::list ? TL_LIST_CAP : TL_EMIT_CAP;
 }
+#ifndef TL_LIST_COALESCED
+#define TL_LIST_COALESCED 0  // list mode: write each flushed batch as consecutive words
+#endif
+#ifndef TL_PACKED_GROUP_EMIT
+#define TL_PACKED_GROUP_EMIT 0  // packed claims: one emission per group of rounds (else per round)
+#endif
 #ifndef TL_SHORT
 #define TL_SHORT 64  // 32 with 1 round in flight: C3 26.7 -> 24.8 ms (more loads in flight for short windows)
 #endif
@@ -429,6 +435,30 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
         if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
         base = __shfl_sync(kFull, base, 0);
       }
+#if TL_LIST_COALESCED
+      if constexpr (MODE == AotMode::list) {
+        // witnesses -> original ids in place, then the batch's 3 * cnt words
+        // written as consecutive words (128 B per store instruction)
+#pragma unroll 4
+        for (uint32_t i = lane_id(); i < cnt; i += 32) {
+          const uint32_t a = st.ebase + 8 * i + 4;
+          st_sm(a, __ldg(P.orig + ld_sm(a)));
+        }
+        __syncwarp();
+        const uint64_t room = P.out_cap > base ? P.out_cap - base : 0, lim = room < cnt ? room : cnt;
+        uint32_t* o = P.out + 3 * base;
+        for (uint32_t j = lane_id(); j < 3 * uint32_t(lim); j += 32) {
+          const uint32_t e = (j * 0xAAABu) >> 17, f = j - 3 * e;  // j / 3 for j < 2^15
+          const uint2 v = ld_sm2(st.ebase + 8 * e);
+          const uint32_t b = v.x & ~kSwapBit;
+          const bool sw = v.x & kSwapBit;
+          o[j] = f == 2 ? v.y : ((f == 0) != sw ? st.a_orig : b);
+        }
+        st.ecount = 0;
+        __syncwarp();
+        return;
+      }
+#endif
 #pragma unroll 4
       for (uint32_t i = lane_id(); i < cnt; i += 32) {
         const uint2 e = ld_sm2(st.ebase + 8 * i);
@@ -481,9 +511,22 @@ __device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, 
 
 // Warp-collective: the hits of one group of U sweep rounds of one list (bit
 // k of `hm` = round k hit on this lane), all with the same neighbour word.
-template <AotMode MODE, int U>
+template <int U>
+struct SameWord {  // one neighbour word for every round (a long sweep of one list)
+  uint32_t w;
+  __device__ __forceinline__ uint32_t operator[](int) const { return w; }
+};
+template <int U>
+struct RoundWords {  // a neighbour word per round (packed claims)
+  const uint32_t (&w)[U];
+  __device__ __forceinline__ uint32_t operator[](int k) const { return w[k]; }
+};
+
+// Warp-collective: the hits of one group of U probe rounds (bit k of `hm` =
+// round k hit on this lane); bw[k] = the neighbour word of round k.
+template <AotMode MODE, int U, typename Words>
 __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint32_t hm, const uint32_t (&x)[U],
-                                           uint32_t bw) {
+                                           const Words& bw) {
   static_assert(32 * U <= emit_cap<MODE>(), "a group's hits must fit the staging buffer");
   const uint32_t lane = lane_id();
   const uint32_t c = __popc(hm);
@@ -500,7 +543,7 @@ __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     if ((hm >> k) & 1u) {
-      st_sm2(slot, bw, x[k]);
+      st_sm2(slot, bw[k], x[k]);
       slot += 8;
     }
   }
@@ -567,12 +610,21 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       if constexpr (MODE != AotMode::count) oo[k] = __shfl_sync(kFull, b_orig, i);
       x[k] = q < total ? __ldg(P.col + obm + q) : kEmpty;
     }
+    uint32_t hm = 0;
 #pragma unroll
     for (int k = 0; k < kSU; ++k) {
       const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
       if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
+#if TL_PACKED_GROUP_EMIT
+      if constexpr (MODE != AotMode::count) hm |= hit << k;
+#else
       if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, oo[k], x[k]);
+#endif
     }
+#if TL_PACKED_GROUP_EMIT
+    if constexpr (MODE != AotMode::count) emit_group<MODE, kSU>(st, P, hm, x, RoundWords<kSU>{oo});
+#endif
+    (void)hm;
   }
 
   // ---- long claims: the whole warp sweeps one list, U rounds of 32
@@ -612,7 +664,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
         hits += hit;
         if constexpr (MODE != AotMode::count) hm |= hit << k;
       }
-      if constexpr (MODE != AotMode::count) emit_group<MODE, U>(st, P, hm, x, oj);
+      if constexpr (MODE != AotMode::count) emit_group<MODE, U>(st, P, hm, x, SameWord<U>{oj});
       p += 32 * U;
       rem -= 32 * U;
       if (__any_sync(kFull, over)) break;
