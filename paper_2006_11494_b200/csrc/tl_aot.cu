@@ -118,12 +118,6 @@ template <AotMode MODE>
 constexpr int emit_cap() {
   return MODE == AotMode::list ? TL_LIST_CAP : TL_EMIT_CAP;
 }
-#ifndef TL_LIST_COALESCED
-#define TL_LIST_COALESCED 0  // list mode: write each flushed batch as consecutive words
-#endif
-#ifndef TL_PACKED_GROUP_EMIT
-#define TL_PACKED_GROUP_EMIT 0  // packed claims: one emission per group of rounds (else per round)
-#endif
 #ifndef TL_SHORT
 #define TL_SHORT 64  // 32 with 1 round in flight: C3 26.7 -> 24.8 ms (more loads in flight for short windows)
 #endif
@@ -169,11 +163,6 @@ struct Params {
 extern __shared__ uint32_t dsmem[];  // dynamic shared memory, addressed by word offset
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t shift) { return (x * 0x9E3779B1u) >> shift; }
 
 // Shared memory is addressed with 32-bit shared::cta byte addresses through
@@ -435,30 +424,6 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
         if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
         base = __shfl_sync(kFull, base, 0);
       }
-#if TL_LIST_COALESCED
-      if constexpr (MODE == AotMode::list) {
-        // witnesses -> original ids in place, then the batch's 3 * cnt words
-        // written as consecutive words (128 B per store instruction)
-#pragma unroll 4
-        for (uint32_t i = lane_id(); i < cnt; i += 32) {
-          const uint32_t a = st.ebase + 8 * i + 4;
-          st_sm(a, __ldg(P.orig + ld_sm(a)));
-        }
-        __syncwarp();
-        const uint64_t room = P.out_cap > base ? P.out_cap - base : 0, lim = room < cnt ? room : cnt;
-        uint32_t* o = P.out + 3 * base;
-        for (uint32_t j = lane_id(); j < 3 * uint32_t(lim); j += 32) {
-          const uint32_t e = (j * 0xAAABu) >> 17, f = j - 3 * e;  // j / 3 for j < 2^15
-          const uint2 v = ld_sm2(st.ebase + 8 * e);
-          const uint32_t b = v.x & ~kSwapBit;
-          const bool sw = v.x & kSwapBit;
-          o[j] = f == 2 ? v.y : ((f == 0) != sw ? st.a_orig : b);
-        }
-        st.ecount = 0;
-        __syncwarp();
-        return;
-      }
-#endif
 #pragma unroll 4
       for (uint32_t i = lane_id(); i < cnt; i += 32) {
         const uint2 e = ld_sm2(st.ebase + 8 * i);
@@ -493,19 +458,6 @@ __device__ __forceinline__ void begin_record(Lane<MODE>& st, const Params& P, ui
     const uint32_t a = __ldg(P.orig + l);
     if (a != st.a_orig && st.ecount) flush_emits(st, P);
     st.a_orig = a;
-  }
-}
-
-// Warp-collective: every lane calls it once per packed probe round (hash /
-// list modes; counters are kept by the caller).  `bw` = neighbour id | swap.
-template <AotMode MODE>
-__device__ __forceinline__ void emit(Lane<MODE>& st, const Params& P, bool hit, uint32_t bw, uint32_t w) {
-  const unsigned hm = __ballot_sync(kFull, hit);
-  if (hm) {
-    const uint32_t k = __popc(hm);
-    if (st.ecount + k > emit_cap<MODE>()) flush_emits(st, P);
-    if (hit) st_sm2(st.ebase + 8 * (st.ecount + __popc(hm & lanemask_lt())), bw, w);
-    st.ecount += k;
   }
 }
 
@@ -615,15 +567,9 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     for (int k = 0; k < kSU; ++k) {
       const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
       if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
-#if TL_PACKED_GROUP_EMIT
       if constexpr (MODE != AotMode::count) hm |= hit << k;
-#else
-      if constexpr (MODE != AotMode::count) emit(st, P, hit != 0, oo[k], x[k]);
-#endif
     }
-#if TL_PACKED_GROUP_EMIT
     if constexpr (MODE != AotMode::count) emit_group<MODE, kSU>(st, P, hm, x, RoundWords<kSU>{oo});
-#endif
     (void)hm;
   }
 
