@@ -122,14 +122,20 @@ constexpr int emit_cap() {
 #define TL_SHORT 64  // 32 with 1 round in flight: C3 26.7 -> 24.8 ms (more loads in flight for short windows)
 #endif
 constexpr uint32_t kShort = TL_SHORT;  // claims of at most this length are packed
-constexpr uint64_t kTaskMin = 4096;    // minimum work per warp task (adaptive: ~64 tasks per warp)
+#ifndef TL_TASK_MIN
+#define TL_TASK_MIN 4096
+#endif
+#ifndef TL_KAPPA
+#define TL_KAPPA 8
+#endif
+constexpr uint64_t kTaskMin = TL_TASK_MIN;  // minimum work per warp task (adaptive: ~64 tasks per warp)
 #ifndef TL_CTA_TASK_SCALE
 #define TL_CTA_TASK_SCALE 8
 #endif
 constexpr uint64_t kCtaTaskScale = TL_CTA_TASK_SCALE;  // a CTA record holds kCtaTaskScale warp tasks of work
 constexpr uint64_t kBeta = 2;    // staging weight per N+(l) element
 constexpr uint64_t kGamma = 64;  // per-record overhead
-constexpr uint64_t kKappa = 8;   // per-claim overhead (scheduling and the multi-GPU cut)
+constexpr uint64_t kKappa = TL_KAPPA;  // per-claim overhead (scheduling and the multi-GPU cut)
 
 // One unit of work: the claims [cb, ce) of pivot l, whose out-list is
 // col[lb, lb + dl).
