@@ -34,6 +34,7 @@ extern "C" {
 #define TL_EPARSE 8   /* ParseError (graph.hpp:89-96): the message starts with "line N: " */
 #define TL_ELENGTH 9  /* std::length_error                                            */
 #define TL_EIO 10     /* std::runtime_error (cannot open / read a file)              */
+#define TL_ECANCELED 11 /* a batch callback returned non-zero: the run stopped        */
 
 #define TL_API __attribute__((visibility("default")))
 
@@ -162,8 +163,10 @@ TL_API int tl_aot_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* sta
  * Writes the emissions of this part as uint32 triples: raw role order
  * (pivot, neighbor, witness) of engine.hpp:256/:269 when canonical == 0, or the
  * sorted canonical (a<b<c) set (canonicalize_emissions, engine.cpp:51-57) when
- * canonical != 0.  triples may be NULL to only count; otherwise cap must be at
- * least the emission count (TL_ECAPACITY otherwise; stats are still filled). */
+ * canonical != 0.  triples == NULL only counts (one counting pass, whose
+ * emission count is cached on the handle to size the listing call); otherwise
+ * one listing pass runs (plus a counting pass when no count is cached) and cap
+ * must be at least the emission count (TL_ECAPACITY otherwise). */
 TL_API int tl_aot_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
                        int canonical, tl_stats* stats);
 
@@ -178,6 +181,32 @@ TL_API int tl_run_count(tl_oriented* og, const tl_run_options* opt, tl_stats* st
 TL_API int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats);
 TL_API int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap,
                        int canonical, tl_stats* stats);
+
+/* run_parallel(algo, g, cfg, SinkFactory) / run_algorithm(algo, g, sink) with an
+ * arbitrary sink (parallel.hpp:25-78, engine.hpp:125-134, :294-304) in
+ * bounded host memory.  The emissions of the run (raw role order, as
+ * tl_run_list with canonical == 0) are produced in batches of at most
+ * batch_triples triples (0 = 2^24): the claim-cost cut splits the run into
+ * consecutive claim ranges, each listed on the device into a batch buffer
+ * (a range that overflows is split in two and listed again), copied to one of
+ * host_buffers (0 = 3, at least 2) pinned host buffers, and handed to
+ * fn(user, triples, count) on the CALLING thread, in order, while the device
+ * already lists the following ranges.  `triples` is valid only during the
+ * call.  fn returning non-zero stops the run (TL_ECANCELED).  Host memory:
+ * host_buffers x 12 x batch_triples bytes; device memory: 2 batch buffers.
+ * opt->part/nparts selects every nparts-th top-level range (multi-GPU: each
+ * rank streams its own share).  stats = the counters summed over the ranges
+ * (identical to tl_run_count's). */
+typedef int (*tl_batch_fn)(void* user, const uint32_t* triples, uint64_t count);
+TL_API int tl_run_list_batches(tl_oriented* og, const tl_run_options* opt, uint64_t batch_triples,
+                               uint32_t host_buffers, tl_batch_fn fn, void* user, tl_stats* stats);
+
+/* The same listing into DEVICE memory of the handle's device (d_triples holds
+ * cap triples): one listing pass, no counting pass and no host copy -- the
+ * emissions stay resident for a device consumer.  Returns TL_ECAPACITY (stats
+ * filled, stats->triangles = the emission count) when cap is too small. */
+TL_API int tl_run_list_device(tl_oriented* og, const tl_run_options* opt, uint32_t* d_triples, uint64_t cap,
+                              int canonical, tl_stats* stats);
 
 /* verify_equivalence's comparison (engine.cpp:82-130) for one orientation,
  * on the device: every algorithm in `algorithms` (TL_ALGO_*) lists its

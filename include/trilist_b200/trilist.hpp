@@ -19,14 +19,18 @@
 
 #include <array>
 #include <compare>
+#include <condition_variable>
 #include <cstdint>
+#include <exception>
 #include <initializer_list>
 #include <iosfwd>
 #include <string_view>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -282,15 +286,119 @@ RunStats device_list(Algorithm algo, const OrientedGraph& g, const RunOptions& o
                      std::vector<std::array<VertexId, 3>>& raw);
 }  // namespace detail
 
+namespace detail {
+/// Batched listing (tl_run_list_batches): the run's emissions, raw role order,
+/// handed to fn(user, triples, count) in batches of at most batch_triples
+/// (0: TRILIST_BATCH_TRIPLES or 2^24) on the calling thread while the device
+/// lists ahead; bounded host memory.  *canceled is set when fn stopped the run.
+using BatchFn = int (*)(void* user, const std::uint32_t* triples, std::uint64_t count);
+RunStats device_batches(Algorithm algo, const OrientedGraph& g, const RunOptions& opt, BatchFn fn, void* user,
+                        bool* canceled);
+
+/// Replays each batch into `workers` sinks: slice w of a batch goes to sink w,
+/// on worker thread w (the calling thread is worker 0) -- run_parallel's one
+/// sink per worker (parallel.hpp:32-35, :55-72).  The first exception a sink
+/// throws stops the run and is rethrown by the caller.
+template <typename Sink>
+class BatchReplayer {
+ public:
+  explicit BatchReplayer(std::vector<Sink>& sinks) : sinks_(sinks), workers_(unsigned(sinks.size())) {
+    for (unsigned w = 1; w < workers_; ++w) threads_.emplace_back([this, w] { loop(w); });
+  }
+  ~BatchReplayer() {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      stop_ = true;
+    }
+    start_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  static int call(void* self, const std::uint32_t* t, std::uint64_t count) {
+    return static_cast<BatchReplayer*>(self)->replay(t, count);
+  }
+  std::exception_ptr error() const { return error_; }
+
+ private:
+  int replay(const std::uint32_t* t, std::uint64_t count) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      batch_ = t;
+      count_ = count;
+      pending_ = workers_ - 1;
+      ++generation_;
+    }
+    start_.notify_all();
+    slice(0);
+    std::unique_lock<std::mutex> lock(mu_);
+    done_.wait(lock, [this] { return pending_ == 0; });
+    return error_ ? 1 : 0;
+  }
+  void slice(unsigned w) {
+    try {
+      const std::uint64_t b = count_ * w / workers_, e = count_ * (w + 1) / workers_;
+      Sink& sink = sinks_[w];
+      for (std::uint64_t i = b; i < e; ++i) sink(batch_[3 * i], batch_[3 * i + 1], batch_[3 * i + 2]);
+    } catch (...) {
+      std::lock_guard<std::mutex> lock(mu_);
+      if (!error_) error_ = std::current_exception();
+    }
+  }
+  void loop(unsigned w) {
+    std::uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        start_.wait(lock, [&] { return stop_ || generation_ != seen; });
+        if (stop_) return;
+        seen = generation_;
+      }
+      slice(w);
+      {
+        std::lock_guard<std::mutex> lock(mu_);
+        --pending_;
+      }
+      done_.notify_all();
+    }
+  }
+  std::vector<Sink>& sinks_;
+  unsigned workers_;
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable start_, done_;
+  const std::uint32_t* batch_ = nullptr;
+  std::uint64_t count_ = 0, generation_ = 0;
+  unsigned pending_ = 0;
+  bool stop_ = false;
+  std::exception_ptr error_;
+};
+
+template <typename Sink>
+RunStats replay_batches(Algorithm algo, const OrientedGraph& g, std::vector<Sink>& sinks, const RunOptions& opt) {
+  BatchReplayer<Sink> rep(sinks);
+  bool canceled = false;
+  RunStats s = device_batches(algo, g, opt, &BatchReplayer<Sink>::call, &rep, &canceled);
+  if (rep.error()) std::rethrow_exception(rep.error());
+  return s;
+}
+}  // namespace detail
+
+/// run_algorithm (engine.hpp:294-304): NullSink counts; CollectingSink appends
+/// the device list in one copy; any other sink gets every emission (role order
+/// pivot, neighbor, witness) replayed from bounded host batches.
 template <typename Sink>
 RunStats run_algorithm(Algorithm algo, const OrientedGraph& g, Sink&& sink, const RunOptions& opt = {}) {
-  if constexpr (std::is_same_v<std::decay_t<Sink>, NullSink>) {
+  using S = std::decay_t<Sink>;
+  if constexpr (std::is_same_v<S, NullSink>) {
     return detail::device_count(algo, g, opt, 0);
+  } else if constexpr (std::is_same_v<S, CollectingSink>) {
+    return detail::device_list(algo, g, opt, *sink.out);
   } else {
-    std::vector<std::array<VertexId, 3>> raw;
-    RunStats s = detail::device_list(algo, g, opt, raw);
-    for (const auto& t : raw) sink(t[0], t[1], t[2]);  // role order (pivot, neighbor, witness)
-    return s;
+    struct Ref {  // the caller's sink, by reference
+      std::remove_reference_t<Sink>* p;
+      void operator()(VertexId a, VertexId b, VertexId c) { (*p)(a, b, c); }
+    };
+    std::vector<Ref> one{Ref{&sink}};
+    return detail::replay_batches(algo, g, one, opt);
   }
 }
 
@@ -360,8 +468,12 @@ namespace detail {
 void validate(const ParallelConfig& cfg);
 }
 
-/// run_parallel (parallel.hpp:25-78): one device run; the emissions are
-/// handed to the sink of worker 0 (the other workers' sinks see none).
+/// run_parallel (parallel.hpp:25-78): one device run; one sink per worker
+/// from the factory (:32-35).  NullSinks count; other sinks receive the
+/// emissions in bounded host batches, each batch split across the workers'
+/// sinks and replayed on `workers` host threads (the first exception a sink
+/// throws is rethrown, :55-72).  Counters are those of the device run, the
+/// same for any workers/chunk (test_parallel.cpp:11-40).
 template <typename SinkFactory>
 RunStats run_parallel(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg, SinkFactory&& make_sink,
                       const RunOptions& opt = {}) {
@@ -370,7 +482,11 @@ RunStats run_parallel(Algorithm algo, const OrientedGraph& g, const ParallelConf
   std::vector<Sink> sinks;
   sinks.reserve(cfg.workers);
   for (unsigned w = 0; w < cfg.workers; ++w) sinks.push_back(make_sink(w));
-  return run_algorithm(algo, g, sinks[0], opt);
+  if constexpr (std::is_same_v<Sink, NullSink>) {
+    return detail::device_count(algo, g, opt, 0);
+  } else {
+    return detail::replay_batches(algo, g, sinks, opt);
+  }
 }
 
 RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,

@@ -26,7 +26,7 @@ LIB = os.path.join(LIBDIR, "libtrilist_b200.so")
 EXT = os.path.join(PKG, "trilist", "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 CLI = os.path.join(PKG, "bin", "trilist")
 
-CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_verify.cu", "tl_capi.cu"]
+CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_verify.cu", "tl_stream.cu", "tl_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -97,6 +97,21 @@ def build_cli(verbose: bool = False, force: bool = False) -> str:
     return CLI
 
 
+STREAM_CHECK = os.path.join(PKG, "bin", "stream_sink_check")
+
+
+def build_stream_check(verbose: bool = False, force: bool = False) -> str:
+    """tools/stream_sink_check.cpp: a C++ run_parallel caller with a custom
+    (hash) sink over the facade -- the bounded-memory streaming path."""
+    srcs = [os.path.join(ROOT, "tools", "stream_sink_check.cpp"), os.path.join(CSRC, "facade.cpp")]
+    if force or _stale(STREAM_CHECK, srcs + _headers() + [LIB]):
+        os.makedirs(os.path.dirname(STREAM_CHECK), exist_ok=True)
+        _run(["g++", "-O2", "-std=c++20", "-pthread", "-I" + INC, "-I/usr/local/cuda/include"] + srcs +
+             ["-L" + LIBDIR, "-ltrilist_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath,$ORIGIN/../lib", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", STREAM_CHECK], verbose)
+    return STREAM_CHECK
+
+
 VARIANTS = {
     # Small probe regions and a low CTA threshold: small test graphs then
     # reach every probe path (warp/CTA bitmap, rank bitmap, hash, global
@@ -130,6 +145,7 @@ def build(verbose: bool = False, force: bool = False) -> None:
     build_lib(verbose, force)
     build_ext(verbose, force)
     build_cli(verbose, force)
+    build_stream_check(verbose, force)
     for name in VARIANTS:
         build_variant(name, verbose, force)
 

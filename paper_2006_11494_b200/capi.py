@@ -17,7 +17,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TL_LIB_PATH") or os.path.join(PKG, "lib", "libtrilist_b200.so")
 
 (TL_OK, TL_EINVAL, TL_ERANGE, TL_ELOGIC, TL_ECUDA, TL_ENOMEM, TL_ECAPACITY, TL_ENODEV, TL_EPARSE, TL_ELENGTH,
- TL_EIO) = range(11)
+ TL_EIO, TL_ECANCELED) = range(12)
+
+# tl_batch_fn: int (*)(void* user, const uint32_t* triples, uint64_t count)
+BATCH_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint32), C.c_uint64)
 
 # Every symbol include/trilist_b200.h declares (checked by tests/test_cabi_symbols.py).
 EXPORTS = (
@@ -26,7 +29,7 @@ EXPORTS = (
     "tl_graph_from_pairs", "tl_graph_free", "tl_graph_info", "tl_graph_degrees", "tl_graph_csr",
     "tl_graph_from_text", "tl_graph_from_file", "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
     "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list",
-    "tl_run_count", "tl_run_hash", "tl_run_list", "tl_verify", "tl_degeneracy_order", "tl_random_order",
+    "tl_run_count", "tl_run_hash", "tl_run_list", "tl_run_list_device", "tl_run_list_batches", "tl_verify", "tl_degeneracy_order", "tl_random_order",
     "tl_brute_force",
 )
 
@@ -131,6 +134,9 @@ def lib() -> C.CDLL:
     L.tl_run_count.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_run_hash.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
     L.tl_run_list.argtypes = [vp, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int, C.POINTER(TlStats)]
+    L.tl_run_list_batches.argtypes = [vp, C.POINTER(TlRunOptions), C.c_uint64, C.c_uint32, BATCH_FN, vp,
+                                      C.POINTER(TlStats)]
+    L.tl_run_list_device.argtypes = [vp, C.POINTER(TlRunOptions), vp, C.c_uint64, C.c_int, C.POINTER(TlStats)]
     L.tl_verify.argtypes = [vp, u32p, C.c_uint32, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.c_int,
                             C.POINTER(TlVerifyResult), u64p]
     L.tl_degeneracy_order.argtypes = [vp, u32p]
@@ -384,3 +390,36 @@ class DeviceOriented:
         out = np.empty((max(st.triangles, 1), 3), np.uint32)
         _check(fn(self._h, C.byref(o), _p32(out), st.triangles, int(canonical), C.byref(st)))
         return st.as_dict(), out[: st.triangles]
+
+    def list_batches(self, fn, batch_triples=0, host_buffers=0, skip_negative=False, part=0, nparts=1, stream=0,
+                     algo="aot", reuse=False) -> dict:
+        """tl_run_list_batches: fn((k, 3) uint32 array view, valid during the
+        call) per batch; fn returning True stops the run (TL_ECANCELED)."""
+        err = []
+
+        def cb(_user, ptr, count):
+            try:
+                arr = np.ctypeslib.as_array(ptr, shape=(int(count) * 3,)).reshape(-1, 3)
+                return 1 if fn(arr) else 0
+            except BaseException as e:  # noqa: BLE001 -- re-raised after the run
+                err.append(e)
+                return 1
+
+        st = TlStats()
+        o = run_options(skip_negative, part, nparts, stream, algo, reuse)
+        rc = lib().tl_run_list_batches(self._h, C.byref(o), batch_triples, host_buffers, BATCH_FN(cb), None,
+                                       C.byref(st))
+        if err:
+            raise err[0]
+        _check(rc)
+        return st.as_dict()
+
+    def list_device(self, d_triples: int, cap: int, canonical=False, skip_negative=False, part=0, nparts=1,
+                    stream=0, algo="aot", reuse=False) -> dict:
+        """tl_run_list_device: one listing pass into device memory d_triples
+        (cap uint32 triples on this handle's device); returns the stats."""
+        st = TlStats()
+        o = run_options(skip_negative, part, nparts, stream, algo, reuse)
+        _check(lib().tl_run_list_device(self._h, C.byref(o), C.c_void_p(d_triples), cap, int(canonical),
+                                        C.byref(st)))
+        return st.as_dict()

@@ -6,6 +6,7 @@
 #include "trilist_b200/trilist.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <charconv>
 #include <cstring>
 #include <istream>
@@ -548,6 +549,27 @@ RunStats device_list(Algorithm algo, const OrientedGraph& g, const RunOptions& o
   static_assert(sizeof(std::array<VertexId, 3>) == 12, "triple layout");
   check(tl_run_list(g.handle(), &o, reinterpret_cast<std::uint32_t*>(raw.data() + base), s.triangles, 0, &s),
         "list run");
+  RunStats r = to_run_stats(s);
+  relayout_table_builds(g, opt, algo, r);
+  return r;
+}
+
+RunStats device_batches(Algorithm algo, const OrientedGraph& g, const RunOptions& opt, BatchFn fn, void* user,
+                        bool* canceled) {
+  require_device_algorithm(algo);
+  assert_layout(algo, g);
+  if (canceled) *canceled = false;
+  if (empty_handle(g)) return RunStats{};
+  tl_run_options o = options_for(algo, opt);
+  std::uint64_t batch = 0;  // 0: the library's default (2^24 triples = 192 MiB per host buffer)
+  if (const char* e = std::getenv("TRILIST_BATCH_TRIPLES")) batch = std::strtoull(e, nullptr, 10);
+  tl_stats s;
+  const int rc = tl_run_list_batches(g.handle(), &o, batch, 0, fn, user, &s);
+  if (rc == TL_ECANCELED) {
+    if (canceled) *canceled = true;
+    return RunStats{};
+  }
+  check(rc, "batched listing");
   RunStats r = to_run_stats(s);
   relayout_table_builds(g, opt, algo, r);
   return r;

@@ -187,6 +187,17 @@ __device__ __forceinline__ void st_sm(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void red_or_sm(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
+__device__ __forceinline__ void red_add_sm64(uint32_t a, unsigned long long v) {
+  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v));
+}
+// Per-warp count of the traversal ids the kernel actually loads (probes left
+// after the rank-window pruning and the in-kernel early exit): one shared
+// 64-bit word per warp, added to by lane 0 once per packed round group / long
+// list, folded into the run's counters at the end.
+__device__ __forceinline__ uint32_t exec_addr() {
+  __shared__ unsigned long long s_exec[32];
+  return static_cast<uint32_t>(__cvta_generic_to_shared(s_exec)) + 8u * (threadIdx.x >> 5);
+}
 __device__ __forceinline__ uint32_t cas_sm(uint32_t a, uint32_t cmp, uint32_t v) {
   uint32_t old;
   asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(v));
@@ -547,6 +558,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   const uint32_t excl = incl - slen;
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   const uint64_t bm = b - excl;  // element q of the packed stream: col[bm(owner) + q]
+  if (lane == 0 && total) red_add_sm64(exec_addr(), total);
 #ifndef TL_SHORT_UNROLL
 #define TL_SHORT_UNROLL 4
 #endif
@@ -622,6 +634,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       if (__any_sync(kFull, over)) break;
     }
     if (nj) st.neg += hits; else st.pos += hits;
+    if (lane == 0) red_add_sm64(exec_addr(), min(lj, uint32_t(int(lj) - rem)));  // ids loaded before the exit
   }
 }
 
@@ -637,6 +650,9 @@ __device__ __forceinline__ void reduce_and_flush(Lane<MODE>& st, const Params& P
     v[3] ^= __shfl_xor_sync(kFull, v[3], o);
   }
   if (lane_id() == 0) {
+    const unsigned long long ex = *reinterpret_cast<volatile unsigned long long*>(
+        __cvta_shared_to_generic(exec_addr()));
+    if (ex) atomicAdd(P.acc + kExec, ex);
     if (v[0]) atomicAdd(P.acc + kPos, v[0]);
     if (v[1]) atomicAdd(P.acc + kNeg, v[1]);
     if (v[2]) atomicAdd(P.acc + kHsum, v[2]);
@@ -798,6 +814,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
+  if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr())) = 0ull;
   Lane<MODE> st;
   st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (2 * emit_cap<MODE>()));
   __syncthreads();
@@ -1263,7 +1280,11 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   const uint64_t ccb = cb, cce = ce;
   const uint32_t cpb = pb, cpe = pe;
   const char* split_mode = getenv("TL_SPLIT_MODE");
-  const bool interleave = !whole && !(split_mode && std::string(split_mode) == "range");
+  // cf merge runs its counter cut's own edges (range mode), so a part's
+  // merge comparisons (per-edge pass minus the part's triangles) are over one
+  // edge set; it is a comparison kernel, not the balanced hot path.
+  const bool interleave = !whole && !spec.range && !(split_mode && std::string(split_mode) == "range") &&
+                          spec.algo != Algo::cf_merge;
   if (interleave) {
     cb = 0;
     ce = m;
@@ -1415,14 +1436,15 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   unsigned long long h[kAccN];
   uint64_t wcb = 0, wce = 0;
   TL_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-  TL_CUDA(cudaMemcpyAsync(&wcb, CP.p + cb, 8, cudaMemcpyDeviceToHost, s));
-  TL_CUDA(cudaMemcpyAsync(&wce, CP.p + ce, 8, cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaMemcpyAsync(&wcb, CP.p + ccb, 8, cudaMemcpyDeviceToHost, s));  // this part's windows (the cut)
+  TL_CUDA(cudaMemcpyAsync(&wce, CP.p + cce, 8, cudaMemcpyDeviceToHost, s));
   TL_CUDA(cudaStreamSynchronize(s));
   TL_CUDA(cudaEventElapsedTime(&r.prep_ms, ev[0], ev[1]));
   TL_CUDA(cudaEventElapsedTime(&r.list_ms, ev[1], ev[2]));
   r.positive = h[kPos];
   r.negative = h[kNeg];
-  r.executed = wce - wcb;  // probes left after the rank-window pruning of each list
+  r.executed = h[kExec];  // traversal ids loaded (after the rank-window pruning and the early exit)
+  r.windowed = CP.p ? wce - wcb : 0;
   if (!logical_from_cost) r.logical = h[kLogical];
   r.hash_sum = h[kHsum];
   r.hash_xor = h[kHxor];

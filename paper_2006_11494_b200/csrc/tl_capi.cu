@@ -85,7 +85,14 @@ void ensure_device_setup(int device) {
   if (device < 0 || device >= 64 || done[device]) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t threshold = ~0ull;  // keep freed blocks cached across calls
+    // keep freed blocks cached across calls (per-run task buffers, an e2e
+    // upload's working set), but never more than a quarter of the device:
+    // at each synchronisation the pool releases what it holds beyond that,
+    // so orient()'s m-sized sort temporaries go back to the device and a
+    // PyTorch allocator in the same process still sees them as free.
+    size_t free_b = 0, total_b = 0;
+    uint64_t threshold = 16ull << 30;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && total_b) threshold = total_b / 4;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
   }
   cudaGetLastError();
@@ -441,6 +448,43 @@ static void run_checked(tl_oriented* og, const tl_run_options* opt, tlb::AotMode
   tlb::fill_stats_from(r, stats);
 }
 
+// The emission count of a run (sizes the output): cached per orientation and
+// claim set, else one counting pass, whose stats are returned in *counted.
+static uint64_t emission_count(tl_oriented* og, const tlb::RunSpec& count_spec, cudaStream_t s,
+                               tlb::AotResult* counted) {
+  auto key = cache_key(count_spec);
+  auto it = og->tri_cache.find(key);
+  if (it != og->tri_cache.end() && !counted) return it->second;
+  tlb::AotResult c = tlb::aot_run(*og, count_spec, s, nullptr, 0);
+  og->tri_cache[key] = c.triangles;
+  if (counted) *counted = c;
+  return c.triangles;
+}
+
+// One listing pass into device memory d_out (cap triples), canonicalised and
+// sorted when asked.  Returns the emission count; TL_ECAPACITY (stats still
+// filled) when it exceeds cap.
+static uint64_t list_into(tl_oriented* og, tlb::RunSpec sp, cudaStream_t s, uint32_t* d_out, uint64_t cap,
+                          int canonical, tl_stats* stats) {
+  sp.mode = tlb::AotMode::list;
+  tlb::AotResult r = tlb::aot_run(*og, sp, s, d_out, cap);
+  const uint64_t T = r.emitted;
+  TL_REQUIRE(T == r.triangles, TL_ELOGIC, "emission count disagrees with the triangle counters");
+  tlb::fill_stats_from(r, stats);
+  sp.mode = tlb::AotMode::count;
+  og->tri_cache[cache_key(sp)] = T;
+  if (T > cap) {
+    TL_CUDA(cudaStreamSynchronize(s));
+    throw tlb::TlError(TL_ECAPACITY, "output capacity " + std::to_string(cap) + " < " + std::to_string(T) +
+                                         " triangles");
+  }
+  if (canonical && T) {
+    tlb::canonicalize_triples(d_out, T, s);
+    tlb::sort_triples(d_out, T, og->nb, s);
+  }
+  return T;
+}
+
 static void list_checked(tl_oriented* og, const tl_run_options* opt, bool any_algorithm, uint32_t* triples,
                          uint64_t cap, int canonical, tl_stats* stats) {
   TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
@@ -448,36 +492,32 @@ static void list_checked(tl_oriented* og, const tl_run_options* opt, bool any_al
   tlb::RunSpec sp = spec_of(o, tlb::AotMode::count, any_algorithm);
   tlb::DeviceGuard guard(og->device);
   cudaStream_t s = pick_stream(o.stream, og->stream);
-  auto key = cache_key(sp);
-  auto it = og->tri_cache.find(key);
-  uint64_t expect;
-  if (it == og->tri_cache.end()) {
-    tlb::AotResult c = tlb::aot_run(*og, sp, s, nullptr, 0);
-    expect = c.triangles;
-    og->tri_cache[key] = expect;
-  } else {
-    expect = it->second;
+  if (!triples) {  // only count (trilist_b200.h): one counting pass, cached for the sizing call
+    tlb::AotResult c;
+    emission_count(og, sp, s, &c);
+    tlb::fill_stats_from(c, stats);
+    return;
   }
+  const uint64_t expect = emission_count(og, sp, s, nullptr);
+  if (cap < expect)
+    throw tlb::TlError(TL_ECAPACITY, "output capacity " + std::to_string(cap) + " < " + std::to_string(expect) +
+                                         " triangles");
   tlb::DBuf<uint32_t> d_out;
   d_out.alloc(std::max<uint64_t>(3 * expect, 3), s);
-  sp.mode = tlb::AotMode::list;
-  tlb::AotResult r = tlb::aot_run(*og, sp, s, d_out.p, expect);
-  const uint64_t T = r.emitted;
-  TL_REQUIRE(T == r.triangles, TL_ELOGIC, "emission count disagrees with the triangle counters");
-  TL_REQUIRE(T <= expect, TL_ELOGIC, "listing emitted more triangles than the counting pass");
-  if (canonical && T) {
-    tlb::canonicalize_triples(d_out.p, T, s);
-    tlb::sort_triples(d_out.p, T, og->nb, s);
-  }
-  tlb::fill_stats_from(r, stats);
-  if (triples) {
-    if (cap < T) {
-      TL_CUDA(cudaStreamSynchronize(s));
-      throw tlb::TlError(TL_ECAPACITY, "output capacity " + std::to_string(cap) + " < " + std::to_string(T) +
-                                           " triangles");
-    }
-    if (T) TL_CUDA(cudaMemcpyAsync(triples, d_out.p, sizeof(uint32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
-  }
+  const uint64_t T = list_into(og, sp, s, d_out.p, expect, canonical, stats);
+  if (T) TL_CUDA(cudaMemcpyAsync(triples, d_out.p, sizeof(uint32_t) * 3 * T, cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaStreamSynchronize(s));
+}
+
+static void list_device_checked(tl_oriented* og, const tl_run_options* opt, uint32_t* d_triples, uint64_t cap,
+                                int canonical, tl_stats* stats) {
+  TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
+  TL_REQUIRE(d_triples || cap == 0, TL_EINVAL, "d_triples is NULL");
+  tl_run_options o = opt ? *opt : defaults();
+  tlb::RunSpec sp = spec_of(o, tlb::AotMode::count, true);
+  tlb::DeviceGuard guard(og->device);
+  cudaStream_t s = pick_stream(o.stream, og->stream);
+  list_into(og, sp, s, d_triples, cap, canonical, stats);
   TL_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -505,6 +545,24 @@ int tl_run_hash(tl_oriented* og, const tl_run_options* opt, tl_stats* stats) {
 int tl_run_list(tl_oriented* og, const tl_run_options* opt, uint32_t* triples, uint64_t cap, int canonical,
                 tl_stats* stats) {
   return guarded([&] { list_checked(og, opt, true, triples, cap, canonical, stats); });
+}
+
+int tl_run_list_batches(tl_oriented* og, const tl_run_options* opt, uint64_t batch_triples, uint32_t host_buffers,
+                        tl_batch_fn fn, void* user, tl_stats* stats) {
+  return guarded([&] {
+    TL_REQUIRE(og, TL_EINVAL, "oriented graph is NULL");
+    tl_run_options o = opt ? *opt : defaults();
+    tlb::RunSpec sp = spec_of(o, tlb::AotMode::list, true);
+    tlb::DeviceGuard guard(og->device);
+    tlb::AotResult r = tlb::list_batches(*og, sp, pick_stream(o.stream, og->stream), batch_triples, host_buffers, fn,
+                                         user);
+    tlb::fill_stats_from(r, stats);
+  });
+}
+
+int tl_run_list_device(tl_oriented* og, const tl_run_options* opt, uint32_t* d_triples, uint64_t cap, int canonical,
+                       tl_stats* stats) {
+  return guarded([&] { list_device_checked(og, opt, d_triples, cap, canonical, stats); });
 }
 
 int tl_verify(tl_oriented* og, const uint32_t* algorithms, uint32_t nalgos, const tl_run_options* opt,

@@ -137,7 +137,7 @@ enum class AotMode { count = 0, hash = 1, list = 2 };
 // The reference's four kernels (engine.hpp:18), numbered as TL_ALGO_*.
 enum class Algo : uint32_t { aot = 0, cf_merge = 1, cf_hash = 2, kclist3 = 3 };
 struct AotResult {
-  uint64_t positive = 0, negative = 0, executed = 0, logical = 0;
+  uint64_t positive = 0, negative = 0, executed = 0, logical = 0, windowed = 0;
   uint64_t hash_sum = 0, hash_xor = 0, emitted = 0, tasks = 0, table_builds = 0, launches = 0;
   // RunStats as the reference reports them for the algorithm (engine.hpp:28-36)
   uint64_t triangles = 0, probes = 0, merge_comparisons = 0, report_positive = 0, report_negative = 0;
@@ -149,10 +149,19 @@ struct RunSpec {
   bool skip_negative = false;  // RunOptions::aot_skip_negative_phase (aot only)
   bool reuse = false;          // RunOptions::cf_hash_reuse_last_table (cf-hash only)
   uint32_t part = 0, nparts = 1;
+  bool range = false;          // run the cost cut's own claim range (no interleaving): batched listing
 };
 // out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).
 AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
 void fill_stats_from(const AotResult& r, tl_stats* st);  // tl_capi.cu
+
+// ---- tl_stream.cu ----
+// Batched listing (tl_run_list_batches): emissions of `spec` in batches of at
+// most batch_triples, handed in order to fn on the calling thread while an
+// internal thread keeps the device listing ahead into a ring of pinned host
+// buffers.  Returns the summed run counters.
+AotResult list_batches(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint64_t batch_triples,
+                       uint32_t host_buffers, tl_batch_fn fn, void* user);
 
 // ---- tl_verify.cu ----
 void verify_algorithms(tl_oriented& og, const uint32_t* algos, uint32_t nalgos, const RunSpec& base,

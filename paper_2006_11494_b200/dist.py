@@ -6,7 +6,8 @@ edges, cut at equal shares of the claim-cost prefix (csrc/tl_aot.cu k_split).
 The only exchange is the reduction of the per-part results:
 
 * sum (NCCL all-reduce, int64 wraps mod 2^64) of triangles, positive,
-  negative, probes, probes_executed, table_builds and hash_sum;
+  negative, probes, probes_executed, table_builds, merge_comparisons and
+  hash_sum;
 * xor of hash_xor -- NCCL has no XOR op, so the per-rank words are
   all-gathered and folded;
 * listing offsets: all-gather of per-rank triangle counts -> exclusive scan ->
@@ -20,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 SUM_KEYS = ("triangles", "positive_triangles", "negative_triangles", "probes", "probes_executed",
-            "table_builds", "hash_sum")
+            "table_builds", "merge_comparisons", "hash_sum")
 MASK64 = (1 << 64) - 1
 
 

@@ -4,6 +4,8 @@ Every case compares the CUDA path with the CPU checkers on the same seeded
 inputs: the C restatement (oracle/trilist_oracle.c) and the reference library
 itself (oracle/_ref).  Integer work => bit-exact equality everywhere.
 """
+import collections
+
 import numpy as np
 import pytest
 
@@ -66,6 +68,10 @@ def check_graph(n, pairs, rank=None, skip_negative=False):
     _, canon = do.list(canonical=True, skip_negative=skip_negative)
     assert np.array_equal(canon, O.canonical_sorted(raw))
     return st
+
+
+def multiset(a):
+    return collections.Counter(map(tuple, np.asarray(a).reshape(-1, 3).tolist()))
 
 
 def test_device_present():
@@ -195,7 +201,7 @@ def test_partitions_sum_to_whole(nparts):
     do = capi.DeviceGraph.from_pairs(pairs, 1 << 14).orient()
     whole = do.hash()
     acc = dict(triangles=0, probes=0, table_builds=0, positive_triangles=0, negative_triangles=0,
-               hash_sum=0, hash_xor=0)
+               probes_executed=0, hash_sum=0, hash_xor=0)
     lists = []
     for p in range(nparts):
         h = do.hash(part=p, nparts=nparts)
@@ -212,6 +218,73 @@ def test_partitions_sum_to_whole(nparts):
     merged = np.concatenate(lists)
     merged = merged[np.lexsort((merged[:, 2], merged[:, 1], merged[:, 0]))]
     assert np.array_equal(merged, do.list(canonical=True)[1])
+
+
+def test_list_null_only_counts():
+    """tl_run_list with triples == NULL runs one counting pass (trilist_b200.h),
+    and the sized call then runs one listing pass (no second count)."""
+    pairs = O.gen_rmat(9, 12, 16 << 12)
+    do = capi.DeviceGraph.from_pairs(pairs, 1 << 12).orient()
+    cnt = do.count()
+    st = capi.TlStats()
+    o = capi.run_options()
+    capi._check(capi.lib().tl_aot_list(do._h, capi.C.byref(o), None, 0, 0, capi.C.byref(st)))
+    assert st.triangles == cnt["triangles"] and st.kernel_launches == cnt["kernel_launches"]
+    out = np.empty((st.triangles, 3), np.uint32)
+    st2 = capi.TlStats()
+    capi._check(capi.lib().tl_aot_list(do._h, capi.C.byref(o), capi._p32(out), st.triangles, 0, capi.C.byref(st2)))
+    assert st2.triangles == st.triangles and st2.kernel_launches == cnt["kernel_launches"]
+    # device-resident listing: one pass, capacity errors reported with the count
+    import torch
+    buf = torch.empty(3 * st.triangles, dtype=torch.int32, device="cuda")
+    d = do.list_device(buf.data_ptr(), st.triangles, canonical=True)
+    assert d["triangles"] == st.triangles
+    host = buf.cpu().numpy().view(np.uint32).reshape(-1, 3)
+    assert np.array_equal(host, do.list(canonical=True)[1])
+    small = torch.empty(3 * 8, dtype=torch.int32, device="cuda")
+    with pytest.raises(capi.TlError):
+        do.list_device(small.data_ptr(), 8)
+    # probes actually loaded: at most the windows, at most the logical probes
+    assert 0 < cnt["probes_executed"] <= cnt["probes"]
+
+
+@pytest.mark.parametrize("algo", ["aot", "cf", "cf-hash", "kclist"])
+def test_list_batches_cover_the_run(algo):
+    """tl_run_list_batches: bounded batches (many ranges, overflowing ones split)
+    deliver exactly the run's emissions, raw role order, with the run's counters;
+    nparts callers together deliver them once; a callback can stop the run."""
+    pairs = O.gen_rmat(12, 12, 16 << 12)
+    do = capi.DeviceGraph.from_pairs(pairs, 1 << 12).orient()
+    whole, raw = do.list(algo=algo)
+    cnt = do.count(algo=algo)
+    got, sizes = [], []
+
+    def take(a):
+        got.append(a.copy())
+        sizes.append(len(a))
+
+    st = do.list_batches(take, batch_triples=997, algo=algo)
+    assert max(sizes) <= 997 and len(sizes) > 3
+    assert multiset(np.concatenate(got)) == multiset(raw)
+    for k in ("triangles", "probes", "merge_comparisons", "table_builds", "positive_triangles",
+              "negative_triangles", "probes_executed"):
+        assert st[k] == cnt[k], k
+    parts = []
+    for p in range(3):
+        do.list_batches(lambda a: parts.append(a.copy()), batch_triples=2000, part=p, nparts=3, algo=algo)
+    assert multiset(np.concatenate(parts)) == multiset(raw)
+    with pytest.raises(capi.TlError) as e:
+        do.list_batches(lambda a: True, batch_triples=997, algo=algo)
+    assert e.value.code == capi.TL_ECANCELED
+
+    class Boom(Exception):
+        pass
+
+    def bad(a):
+        raise Boom()
+
+    with pytest.raises(Boom):
+        do.list_batches(bad, batch_triples=997, algo=algo)
 
 
 def test_upload_reference_layout_matches_orient():

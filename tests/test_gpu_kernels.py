@@ -92,8 +92,11 @@ def test_partitions_sum_to_whole_every_kernel(nparts):  # test_parallel.cpp:11-4
         for algo in KERNELS:
             whole = og.hash(algo=algo)
             parts = [og.hash(algo=algo, part=p, nparts=nparts) for p in range(nparts)]
-            for k in COUNTERS + ("hash_sum",):
+            for k in COUNTERS + ("hash_sum", "probes_executed"):
                 assert sum(p[k] for p in parts) % (1 << 64) == whole[k], (algo, order, k)
+            # every part's counters are over one edge set (no per-part wrap-around)
+            assert all(p["merge_comparisons"] < (1 << 63) for p in parts), algo
+            assert whole["probes_executed"] <= max(whole["probes"], 1) or algo == "cf", algo
             x = 0
             for p in parts:
                 x ^= p["hash_xor"]
