@@ -225,6 +225,7 @@ def test_list_null_only_counts():
     and the sized call then runs one listing pass (no second count)."""
     pairs = O.gen_rmat(9, 12, 16 << 12)
     do = capi.DeviceGraph.from_pairs(pairs, 1 << 12).orient()
+    do.count()  # builds the orientation's cost prefix once (kept on the handle)
     cnt = do.count()
     st = capi.TlStats()
     o = capi.run_options()
