@@ -113,6 +113,41 @@ constexpr uint64_t kCtaMinWork = TL_CTA_MIN_WORK;  // wide-span pivots below thi
 #ifndef TL_LIST_CTAS
 #define TL_LIST_CTAS 4
 #endif
+// Optional (measured, off): long windows streamed through a per-warp
+// shared-memory ring, so the loads in flight hold no registers and a warp
+// keeps TL_RING_STAGES chunks of TL_RING_WORDS ids in flight while it probes
+// the oldest one.  TL_RING=1: 1-D bulk copies (cp.async.bulk -> UBLKCP, one
+// mbarrier per stage); TL_RING=2: per-thread 16-byte cp.async (LDGSTS, zero
+// fill past the window, commit groups).  On a B200 (tools/sweep.py, C4 count,
+// DESIGN §4): register path 277 ms; bulk ring 432 ms (the TMA engine's
+// per-copy cost caps 512-byte copies near 3 TB/s); LDGSTS ring 348 ms at 4
+// CTAs/SM, 353 ms at 5 CTAs/SM with 4 KB probe regions (register path with
+// the same regions: 288 ms) -- the ring's per-chunk bookkeeping costs more
+// issue slots than the latency it hides.  Parity-tested (TL_RING=1 passed the
+// full -m gpu suite); kept for the record and for other GPUs.
+#ifndef TL_RING
+#define TL_RING 0
+#endif
+#ifndef TL_RING_STAGES
+#define TL_RING_STAGES 3
+#endif
+#ifndef TL_RING_WORDS
+#define TL_RING_WORDS 128  // 512 B per chunk (4 probe rounds)
+#endif
+#ifndef TL_RING_CTAS
+#define TL_RING_CTAS 4
+#endif
+template <AotMode MODE>
+constexpr bool ring_mode() {
+  return TL_RING && MODE == AotMode::count;
+}
+constexpr uint32_t kRingStages = TL_RING_STAGES;
+constexpr uint32_t kRingWords = TL_RING_WORDS;
+constexpr uint32_t kRingBytes = 4 * kRingWords;
+constexpr bool kRingAsync = TL_RING == 2;  // 2: per-thread cp.async (LDGSTS); 1: cp.async.bulk (TMA engine)
+static_assert(!kRingAsync || kRingWords % 128 == 0, "LDGSTS chunks are 128-word multiples");
+static_assert((kRingWords & (kRingWords - 1)) == 0 && kRingWords >= 32 && kRingWords <= 256, "ring chunk size");
+
 // per-warp staging of hits (hash / list modes)
 template <AotMode MODE>
 constexpr int emit_cap() {
@@ -190,6 +225,44 @@ __device__ __forceinline__ void red_or_sm(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void red_add_sm64(uint32_t a, unsigned long long v) {
   asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v));
 }
+// mbarrier + 1-D bulk copy (TMA engine, no tensor map): global -> this CTA's
+// shared memory, completion counted in bytes on the stage's mbarrier.
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TL_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TL_WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(__cvta_generic_to_global(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// Per-thread asynchronous copies (LDGSTS): 16 bytes, the bytes past `bytes`
+// zero-filled; completion tracked per thread by commit groups.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(__cvta_generic_to_global(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Per-warp count of the traversal ids the kernel actually loads (probes left
 // after the rank-window pruning and the in-kernel early exit): one shared
 // 64-bit word per warp, added to by lane 0 once per packed round group / long
@@ -412,6 +485,9 @@ struct Lane {
   uint32_t ebase = 0;   // hash/list: byte address of the per-warp staging buffer
   uint32_t ecount = 0;  // warp-uniform
   uint32_t a_orig = 0;  // the current record's pivot (original id)
+  uint32_t ring = 0;    // ring modes: byte address of the warp's chunk ring
+  uint32_t bars = 0;    //             and of its per-stage mbarriers
+  uint32_t phases = 0;  //             bit s = parity of stage s's next completion
   __device__ __forceinline__ void fold() {
     pos64 += pos;
     neg64 += neg;
@@ -525,6 +601,117 @@ constexpr bool kOverLast() {
   return !(MODE == AotMode::count && U == kUnrollLong);
 }
 
+// Long claims (lanes set in longm) through the warp's chunk ring.  Each
+// window [b, b + len) of col is read as 16-byte-aligned chunks of at most
+// kRingWords words (col is padded by 16 B): the words before b and past the
+// window's end are overwritten with kEmpty (never a hit) before probing.  The
+// chunk stream runs across the batch's long claims, kRingStages chunks ahead
+// of the probing.  No early exit: the windows end at the list's end, and the
+// ids past max N+(l) cost one probe each (measured: windows are nearly tight).
+template <AotMode MODE, typename Probe>
+__device__ __forceinline__ void ring_sweep(const Params& P, const Probe& probe, uint32_t lmax, unsigned longm,
+                                           uint64_t b, uint32_t len, bool neg, Lane<MODE>& st) {
+  const uint32_t lane = lane_id();
+  const uint64_t a0 = b & ~3ull;                                       // 16-byte-aligned chunk origin
+  const uint32_t wtot = uint32_t(((b + len + 3) & ~3ull) - a0);        // words to copy (multiple of 4)
+  const uint32_t nch = (wtot + kRingWords - 1) / kRingWords;           // chunks of this lane's claim
+  // producer cursor: claim lane pj, chunk pc of pn
+  unsigned pm = longm;
+  int pj = __ffs(pm) - 1;
+  uint32_t pc = 0, pn = __shfl_sync(kFull, nch, pj);
+  const uint32_t wend = uint32_t(b + len - a0);                       // one past the window, from a0
+  auto issue = [&](uint32_t slot) {
+    if constexpr (kRingAsync) {
+      if (pj < 0) {
+        cp_async_commit();  // an empty group keeps one group per chunk slot
+        return;
+      }
+      const uint64_t pa = __shfl_sync(kFull, a0, pj);
+      const uint32_t pe = __shfl_sync(kFull, wend, pj);
+#pragma unroll
+      for (uint32_t v = 0; v < kRingWords / 128; ++v) {
+        // lane copies words [w, w + 4) of the window's copy; past the window's
+        // end the bytes are zero-filled (id 0 is never in a probe side: every
+        // out-list holds ids above its owner)
+        const uint32_t w = pc * kRingWords + 128 * v + 4 * lane;
+        const uint32_t nb = w < pe ? min(16u, 4 * (pe - w)) : 0u;
+        cp_async16(st.ring + slot * kRingBytes + 512 * v + 16 * lane, P.col + pa + (nb ? w : 0u), nb);
+      }
+      cp_async_commit();
+    } else {
+      if (pj < 0) return;
+      const uint64_t pa = __shfl_sync(kFull, a0, pj);
+      const uint32_t pw = __shfl_sync(kFull, wtot, pj);
+      if (lane == 0) {
+        const uint32_t words = min(kRingWords, pw - pc * kRingWords);
+        const uint32_t bar = st.bars + 8 * slot;
+        mbar_expect_tx(bar, 4 * words);
+        bulk_g2s(st.ring + slot * kRingBytes, P.col + pa + uint64_t(pc) * kRingWords, 4 * words, bar);
+      }
+    }
+    if (++pc == pn) {
+      pm &= pm - 1;
+      pj = pm ? __ffs(pm) - 1 : -1;
+      pc = 0;
+      pn = __shfl_sync(kFull, nch, pj < 0 ? 0 : pj);
+    }
+  };
+#pragma unroll
+  for (uint32_t i = 0; i < kRingStages; ++i) issue(i);
+  // consumer cursor
+  unsigned cm = longm;
+  int cj = __ffs(cm) - 1;
+  uint32_t cc = 0, hits = 0, s = 0;
+  uint32_t cn = __shfl_sync(kFull, nch, cj), head = __shfl_sync(kFull, uint32_t(b - a0), cj);
+  uint32_t cl = __shfl_sync(kFull, len, cj);
+  bool cneg = __shfl_sync(kFull, neg, cj);
+  while (true) {
+    if constexpr (kRingAsync) {
+      cp_async_wait<kRingStages - 1>();  // this lane's copies of the oldest chunk have landed
+    } else {
+      mbar_wait(st.bars + 8 * s, (st.phases >> s) & 1u);
+      st.phases ^= 1u << s;
+    }
+    const uint32_t wb = cc * kRingWords;                     // chunk origin within the window's copy
+    const uint32_t lo = cc == 0 ? head : 0u;                 // valid words [lo, hi) of this chunk
+    const uint32_t hi = min(kRingWords, head + cl - wb);
+    const uint32_t rounds = (hi + 31) >> 5;
+    const uint32_t sb = st.ring + s * kRingBytes;
+    if constexpr (kRingAsync) {
+      __syncwarp();  // every lane's copies of the chunk are visible to the warp
+      if (lane < lo) st_sm(sb + 4 * lane, kEmpty);
+    } else {
+      if (lane < lo) st_sm(sb + 4 * lane, kEmpty);
+      if (hi + lane < 32 * rounds) st_sm(sb + 4 * (hi + lane), kEmpty);
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t k = 0; k < kRingWords / 32; ++k) {
+      if (k < rounds) {
+        const uint32_t x = ld_sm(sb + 4 * (32 * k + lane));
+        hits += Probe::kRangeChecked ? probe.bit(x) : uint32_t(x <= lmax && probe.test(x));
+      }
+    }
+    if constexpr (!kRingAsync) fence_proxy_async();  // reads / masks of the slot precede the next bulk write
+    __syncwarp();
+    issue(s);
+    s = s + 1 == kRingStages ? 0u : s + 1;
+    if (++cc == cn) {
+      if (cneg) st.neg += hits; else st.pos += hits;
+      if (lane == 0) red_add_sm64(exec_addr(), cl);
+      cm &= cm - 1;
+      if (!cm) break;
+      cj = __ffs(cm) - 1;
+      cc = 0;
+      hits = 0;
+      cn = __shfl_sync(kFull, nch, cj);
+      head = __shfl_sync(kFull, uint32_t(b - a0), cj);
+      cl = __shfl_sync(kFull, len, cj);
+      cneg = __shfl_sync(kFull, neg, cj);
+    }
+  }
+}
+
 // One warp processes claims [base, min(base + 32, ce)) of a pivot against the
 // staged probe side.  All 32 lanes must call it.
 template <AotMode MODE, int U, typename Probe>
@@ -591,10 +778,14 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     (void)hm;
   }
 
+  unsigned longm = __ballot_sync(kFull, len > kShort);
+  if constexpr (ring_mode<MODE>()) {
+    if (longm) ring_sweep<MODE>(P, probe, lmax, longm, b, len, neg, st);
+    return;
+  }
   // ---- long claims: the whole warp sweeps one list, U rounds of 32
   // loads in flight; lists are rank-ascending, so a list is abandoned once a
   // group reaches past max N+(l)
-  unsigned longm = __ballot_sync(kFull, len > kShort);
   while (longm) {
     const int j = __ffs(longm) - 1;
     longm &= longm - 1;
@@ -807,7 +998,7 @@ __device__ __forceinline__ void cta_record(const Params& P, const Rec& R, uint32
 }
 
 template <AotMode MODE, int U>
-__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTAS_PER_SM
+__global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_mode<MODE>() ? TL_RING_CTAS : TL_CTAS_PER_SM)
                                                           : MODE == AotMode::hash ? TL_EMIT_CTAS
                                                                                   : TL_LIST_CTAS) k_aot(Params P) {
   __shared__ unsigned long long s_task;
@@ -817,6 +1008,16 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? TL_CTA
   if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr())) = 0ull;
   Lane<MODE> st;
   st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (2 * emit_cap<MODE>()));
+  if constexpr (ring_mode<MODE>()) {
+    constexpr uint32_t off =
+        (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
+    st.bars = sm_addr(off + warp * 2 * kRingStages);
+    st.ring = sm_addr(off + ((kWarpsPerCta * 2 * kRingStages + 31) & ~31u) + warp * kRingStages * kRingWords);
+    if (lane == 0) {
+      for (uint32_t i = 0; i < kRingStages; ++i) mbar_init(st.bars + 8 * i, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   // ---- phase 1: CTA records
   if (P.ncta) {
@@ -1112,9 +1313,19 @@ int sm_count() {
   return sms > 0 ? sms : 148;
 }
 
+// Dynamic shared memory: the warps' probe regions, then (hash / list) the
+// warps' hit staging, then (ring modes) the stage mbarriers and the rings.
+template <AotMode MODE>
+__host__ __device__ constexpr uint32_t ring_words_offset() {  // 32-word (128 B) aligned
+  return (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
+}
 template <AotMode MODE>
 size_t kernel_smem() {
-  return sizeof(uint32_t) * (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0));
+  uint32_t words = kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0);
+  if (ring_mode<MODE>())
+    words = ring_words_offset<MODE>() + ((kWarpsPerCta * 2 * kRingStages + 31) & ~31u) +
+            kWarpsPerCta * kRingStages * kRingWords;
+  return sizeof(uint32_t) * words;
 }
 
 template <AotMode MODE>

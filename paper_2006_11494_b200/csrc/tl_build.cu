@@ -675,7 +675,7 @@ void finish_orient(tl_oriented& og, DBuf<uint64_t>& dk) {
   cudaStream_t s = og.stream;
   const PhaseClock clk("finish", s);
   const uint64_t m = og.m;
-  og.col.alloc(std::max<uint64_t>(m, 1), s);
+  og.col.alloc(m + 4, s);  // + 16 B: bulk copies of a window round its end up to 16 B
   og.claim_off.alloc(uint64_t(og.n) + 1, s);
   DBuf<uint64_t> scal;
   scal.alloc(4, s);
@@ -882,7 +882,7 @@ void oriented_from_host_csr(tl_oriented& og, uint32_t n, uint64_t m, const uint6
       });
     }
     clk.mark("offsets");
-    og.col.alloc(std::max<uint64_t>(m, 1), s);
+    og.col.alloc(m + 4, s);  // + 16 B: bulk copies of a window round its end up to 16 B
     ckey.alloc(std::max<uint64_t>(m, 1), s);
     val.alloc(std::max<uint64_t>(m, 1), s);
     scal.alloc(4, s);

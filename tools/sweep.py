@@ -33,7 +33,8 @@ def build(specs):
     for p, name, o in procs:
         assert p.wait() == 0, name
         lib = os.path.join(VDIR, f"lib_{name}.so")
-        subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib, o] + objs, check=True)
+        subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib, o] + objs +
+                       ["-Xlinker", "--exclude-libs,ALL", "-lz"], check=True)
         print("built", lib)
 
 
