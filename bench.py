@@ -464,10 +464,36 @@ def run_ours(args):
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without a launcher: start the N ranks here (one
+    process per GPU, torch.distributed.run on 127.0.0.1) and relay their
+    output; rank 0 prints the JSON line.  NCCL's init log (NCCL_DEBUG=INFO,
+    subsystem INIT) stays visible so every rank's communicator can be counted."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mislabelled run",
+              file=sys.stderr, flush=True)
+        return 2
     return run_ours(args)
 
 

@@ -143,7 +143,7 @@ constexpr bool ring_mode() {
 }
 constexpr uint32_t kRingStages = TL_RING_STAGES;
 constexpr uint32_t kRingWords = TL_RING_WORDS;
-constexpr uint32_t kRingBytes = 4 * kRingWords;
+[[maybe_unused]] constexpr uint32_t kRingBytes = 4 * kRingWords;
 constexpr bool kRingAsync = TL_RING == 2;  // 2: per-thread cp.async (LDGSTS); 1: cp.async.bulk (TMA engine)
 static_assert(!kRingAsync || kRingWords % 128 == 0, "LDGSTS chunks are 128-word multiples");
 static_assert((kRingWords & (kRingWords - 1)) == 0 && kRingWords >= 32 && kRingWords <= 256, "ring chunk size");
@@ -225,6 +225,7 @@ __device__ __forceinline__ void red_or_sm(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void red_add_sm64(uint32_t a, unsigned long long v) {
   asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v));
 }
+#pragma nv_diag_suppress 177  // the ring helpers are unused when TL_RING=0
 // mbarrier + 1-D bulk copy (TMA engine, no tensor map): global -> this CTA's
 // shared memory, completion counted in bytes on the stage's mbarrier.
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
@@ -1367,7 +1368,107 @@ uint64_t launch_kernels(const Params& P, bool long_lists, cudaStream_t s) {
 
 }  // namespace
 
+// A run's work: warp records + cost-balanced warp tasks, CTA records.
+struct AotPlan {
+  DBuf<Rec> wrecs, crecs;
+  DBuf<uint2> tasks;
+  uint64_t nw = 0, nc = 0, G = 0;
+};
+
 namespace {
+// Builds the work records of claims [cb, ce) (pivots [pb, pe)) at task size T
+// into `plan` (buffers on stream ps; the temporaries and kernels on s).
+void build_plan(tl_oriented& og, AotPlan& plan, const uint64_t* CP, const uint64_t* claim_off, uint32_t pb,
+                uint32_t pe, uint64_t cb, uint64_t ce, uint64_t T, cudaStream_t ps, cudaStream_t s, bool debug_paths,
+                uint64_t& launches) {
+  const uint32_t np = cb < ce ? pe - pb : 0;
+  if (!np) return;
+  DBuf<uint32_t> nrw, nrc, ow, oc;
+  DBuf<uint64_t> wgt;
+  nrw.alloc(np + 1, s);
+  nrc.alloc(np + 1, s);
+  ow.alloc(np + 1, s);
+  oc.alloc(np + 1, s);
+  k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP, claim_off, og.off.p, og.col.p, pb, np,
+                                                                        cb, ce, T, nrw.p, nrc.p);
+  TL_CUDA(cudaGetLastError());
+  cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrw.p, ow.p, np + 1, s); });
+  cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrc.p, oc.p, np + 1, s); });
+  if (debug_paths) {
+    DBuf<unsigned long long> pst;
+    pst.alloc(48, s);
+    TL_CUDA(cudaMemsetAsync(pst.p, 0, 48 * 8, s));
+    k_path_stats<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP, claim_off, og.off.p, og.col.p, pb, np, cb, ce,
+                                                              pst.p);
+    unsigned long long hp[48];
+    TL_CUDA(cudaMemcpyAsync(hp, pst.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr,
+            "[tl paths] warp-bitmap %llu warp-rank %llu warp-hash %llu cta-bitmap %llu cta-rank %llu cta-hash %llu "
+            "global %llu\n",
+            hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[6]);
+    fprintf(stderr, "[tl span log2 buckets]");
+    for (int b = 0; b < 40; ++b)
+      if (hp[8 + b]) fprintf(stderr, " %d:%llu", b, hp[8 + b]);
+    fprintf(stderr, "\n");
+  }
+  uint32_t tw = 0, tc = 0;
+  TL_CUDA(cudaMemcpyAsync(&tw, ow.p + np, 4, cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaMemcpyAsync(&tc, oc.p + np, 4, cudaMemcpyDeviceToHost, s));
+  TL_CUDA(cudaStreamSynchronize(s));
+  plan.nw = tw;
+  plan.nc = tc;
+  launches += 1 + 2 * 2;
+  // plan buffers are allocated on ps, before the kernels on s use them
+  if (plan.nw) plan.wrecs.alloc(plan.nw, ps);
+  if (plan.nc) plan.crecs.alloc(plan.nc, ps);
+  if (ps != s) {
+    cudaEvent_t e;
+    TL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(e, ps));
+    TL_CUDA(cudaStreamWaitEvent(s, e, 0));
+    cudaEventDestroy(e);
+  }
+  if (plan.nw) {
+    const uint64_t nw = plan.nw;
+    wgt.alloc(nw + 1, s);
+    TL_CUDA(cudaMemsetAsync(wgt.p + nw, 0, 8, s));
+    k_records<<<grid_for(nw, 256, 148u * 32u), 256, 0, s>>>(CP, claim_off, og.off.p, pb, np, cb, ce, nrw.p, ow.p, nw,
+                                                            plan.wrecs.p, wgt.p);
+    TL_CUDA(cudaGetLastError());
+    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, wgt.p, nw + 1, s); });
+    uint64_t total = 0;
+    TL_CUDA(cudaMemcpyAsync(&total, wgt.p + nw, 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+    plan.G = total ? (total - 1) / T + 1 : 0;
+    // the task list is written on s; allocate it there and move ownership to ps after
+    plan.tasks.alloc(std::max<uint64_t>(plan.G, 1), ps);
+    if (ps != s) {
+      cudaEvent_t e;
+      TL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TL_CUDA(cudaEventRecord(e, ps));
+      TL_CUDA(cudaStreamWaitEvent(s, e, 0));
+      cudaEventDestroy(e);
+    }
+    if (plan.G) k_tasks<<<grid_for(plan.G, 256, 148u * 32u), 256, 0, s>>>(wgt.p, uint32_t(nw), plan.G, T, plan.tasks.p);
+    TL_CUDA(cudaGetLastError());
+    launches += 1 + 2 + (plan.G ? 1 : 0);
+  }
+  if (plan.nc) {
+    k_records<<<grid_for(plan.nc, 256, 148u * 32u), 256, 0, s>>>(CP, claim_off, og.off.p, pb, np, cb, ce, nrc.p, oc.p,
+                                                                 plan.nc, plan.crecs.p, nullptr);
+    TL_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (ps != s) {  // the plan's writes are complete before ps may free it
+    cudaEvent_t e;
+    TL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(e, s));
+    TL_CUDA(cudaStreamWaitEvent(ps, e, 0));
+    cudaEventDestroy(e);
+  }
+}
+
 void ensure_forward_claims(tl_oriented& og, cudaStream_t s) {
   if (og.fwd_win.p || og.m == 0) return;
   og.fwd_win.alloc(og.m, og.stream);  // owned by the handle's stream
@@ -1437,7 +1538,11 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
         thrust::make_transform_iterator(thrust::counting_iterator<uint64_t>(0), WindowLength{cwin, m, skip_negative});
     uint64_t* dst = og.cp.p;
     cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, lens, dst, m + 1, s); });
+    TL_CUDA(cudaMemcpyAsync(&og.cp_total, dst + m, 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
     og.cp_key = cp_key;
+    og.cuts.clear();  // cuts and plans belong to the previous claim set's prefix
+    og.plans.clear();
     r.launches += 2;  // scan (init + sweep)
   }
   struct {
@@ -1446,155 +1551,121 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   mark("alloc");
   const bool whole = nparts == 1;
   // logical probes (engine.hpp:250/:264): the orientation's cost model when
-  // the run covers every claim, else a pass over the part's claims
+  // the run covers every claim, else a pass over the part's claims (once per
+  // handle and part: the cut and its counters are cached with it)
   const bool logical_from_cost = whole && !skip_negative;
-  if (logical_from_cost) {
-    r.logical = fwd ? og.cost[1] : og.cost[2];
-  } else if (whole) {
-    k_logical<<<grid_for(m, 256, 148u * 32u), 256, 0, s>>>(cs, og.off.p, 0, m, skip_negative, acc.p + kLogical);
-    TL_CUDA(cudaGetLastError());
-    ++r.launches;
-  }
-  mark("cost+scan");
-  uint64_t cb = 0, ce = m;
-  uint32_t pb = 0, pe = og.n;
-  if (whole) {
-    r.table_builds = m;
-  } else {
-    DBuf<uint64_t> split;
-    split.alloc(8, s);
-    k_split<<<1, 32, 0, s>>>(CP.p, m, claim_off, og.off.p, og.n, part, nparts, split.p);
-    TL_CUDA(cudaGetLastError());
-    uint64_t hs[8];
-    TL_CUDA(cudaMemcpyAsync(hs, split.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaStreamSynchronize(s));
-    cb = hs[0];
-    ce = hs[1];
-    pb = uint32_t(hs[2]);
-    pe = uint32_t(hs[3]);
-    r.table_builds = hs[6];
-    ++r.launches;
-    if (cb < ce) {
-      k_logical<<<grid_for(ce - cb, 256, 148u * 32u), 256, 0, s>>>(cs, og.off.p, cb, ce, skip_negative,
-                                                                 acc.p + kLogical);
-      TL_CUDA(cudaGetLastError());
-      ++r.launches;
-    }
-  }
-
-  // Multi-GPU execution: the cut above attributes the logical-probe and
-  // table-build counters (they only need to partition exactly); with
-  // interleaving (the default) every part then builds the whole graph's work
-  // records and runs every nparts-th task and CTA record, so each GPU gets an
-  // even mix of every probe path.  TL_SPLIT_MODE=range runs the cut's own
-  // claim range instead.
-  const uint64_t ccb = cb, cce = ce;
-  const uint32_t cpb = pb, cpe = pe;
+  // Multi-GPU execution: the cut attributes the logical-probe and table-build
+  // counters (they only need to partition exactly); with interleaving (the
+  // default) every part then works from the whole graph's work records and
+  // runs every nparts-th task and CTA record, so each GPU gets an even mix of
+  // every probe path.  TL_SPLIT_MODE=range runs the cut's own claim range
+  // instead.  cf merge runs its counter cut's own edges (range mode), so a
+  // part's merge comparisons (per-edge pass minus the part's triangles) are
+  // over one edge set; it is a comparison kernel, not the balanced hot path.
   const char* split_mode = getenv("TL_SPLIT_MODE");
-  // cf merge runs its counter cut's own edges (range mode), so a part's
-  // merge comparisons (per-edge pass minus the part's triangles) are over one
-  // edge set; it is a comparison kernel, not the balanced hot path.
   const bool interleave = !whole && !spec.range && !(split_mode && std::string(split_mode) == "range") &&
                           spec.algo != Algo::cf_merge;
-  if (interleave) {
-    cb = 0;
-    ce = m;
-    pb = 0;
-    pe = og.n;
+  const bool cache = !spec.range;  // batched listing walks thousands of ranges once each
+  // ---- the part's cost cut: {cb, ce, pb, pe, table_builds, logical, has_logical, CP[cb], CP[ce]}
+  std::array<uint64_t, 9> cut_local{};
+  std::array<uint64_t, 9>* cutp = nullptr;
+  const auto cut_key = std::make_tuple(cp_key, whole ? 0u : part, whole ? 1u : nparts);
+  if (cache) {
+    auto it = og.cuts.find(cut_key);
+    if (it != og.cuts.end()) cutp = &it->second;
   }
-  // adaptive task size: ~64 warp tasks per resident warp (per part)
-  uint64_t T = kTaskMin;
-  bool long_lists = false;
-  {
-    uint64_t w[2] = {0, 0};
-    TL_CUDA(cudaMemcpyAsync(w, CP.p + cb, 8, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaMemcpyAsync(w + 1, CP.p + ce, 8, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaStreamSynchronize(s));
-    const uint64_t work = (w[1] - w[0]) + kKappa * (ce - cb);
-    // A part's work must not depend on the mode: listing sizes its buffer by
-    // a counting pass over the same part (and the ranks of one job may run
-    // different modes), so a partitioned run sizes tasks for the count
-    // kernel's residency in every mode.
-    int warps = resident_warps<AotMode::count>();
-    if (nparts == 1) {
-      switch (mode) {
-        case AotMode::count: break;
-        case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
-        case AotMode::list: warps = resident_warps<AotMode::list>(); break;
-      }
-    }
-    T = std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
-    long_lists = ce > cb && (w[1] - w[0]) / (ce - cb) >= TL_LONG_WINDOW;
-  }
-
-  mark("task size");
-  const uint32_t np = cb < ce ? pe - pb : 0;
-  DBuf<uint32_t> nrw, nrc, ow, oc;
-  DBuf<Rec> wrecs, crecs;
-  DBuf<uint64_t> wgt;
-  DBuf<uint2> tasks;
-  uint64_t nw = 0, nc = 0, G = 0;
-  if (np) {
-    nrw.alloc(np + 1, s);
-    nrc.alloc(np + 1, s);
-    ow.alloc(np + 1, s);
-    oc.alloc(np + 1, s);
-    k_classify<<<grid_for(uint64_t(np) + 1, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, og.col.p,
-                                                                          pb, np, cb, ce, T, nrw.p, nrc.p);
-    TL_CUDA(cudaGetLastError());
-    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrw.p, ow.p, np + 1, s); });
-    cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, nrc.p, oc.p, np + 1, s); });
-    if (getenv("TL_DEBUG_PATHS")) {
-      DBuf<unsigned long long> ps;
-      ps.alloc(48, s);
-      TL_CUDA(cudaMemsetAsync(ps.p, 0, 48 * 8, s));
-      k_path_stats<<<grid_for(np, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, og.col.p, pb, np, cb,
-                                                                ce, ps.p);
-      unsigned long long hp[48];
-      TL_CUDA(cudaMemcpyAsync(hp, ps.p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+  if (!cutp) {
+    std::array<uint64_t, 9> c{};
+    uint64_t hs[8] = {0, m, 0, og.n, 0, 0, m, 0};
+    DBuf<uint64_t> split;
+    split.alloc(8, s);
+    if (!whole) {
+      k_split<<<1, 32, 0, s>>>(CP.p, m, claim_off, og.off.p, og.n, part, nparts, split.p);
+      TL_CUDA(cudaGetLastError());
+      TL_CUDA(cudaMemcpyAsync(hs, split.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
       TL_CUDA(cudaStreamSynchronize(s));
-      fprintf(stderr,
-              "[tl paths] warp-bitmap %llu warp-rank %llu warp-hash %llu cta-bitmap %llu cta-rank %llu cta-hash %llu "
-              "global %llu\n",
-              hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[6]);
-      fprintf(stderr, "[tl span log2 buckets]");
-      for (int b = 0; b < 40; ++b)
-        if (hp[8 + b]) fprintf(stderr, " %d:%llu", b, hp[8 + b]);
-      fprintf(stderr, "\n");
-    }
-    uint32_t tw = 0, tc = 0;
-    TL_CUDA(cudaMemcpyAsync(&tw, ow.p + np, 4, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaMemcpyAsync(&tc, oc.p + np, 4, cudaMemcpyDeviceToHost, s));
-    TL_CUDA(cudaStreamSynchronize(s));
-    nw = tw;
-    nc = tc;
-    mark("classify");
-    r.launches += 1 + 2 * 2;
-    if (nw) {
-      wrecs.alloc(nw, s);
-      wgt.alloc(nw + 1, s);
-      TL_CUDA(cudaMemsetAsync(wgt.p + nw, 0, 8, s));
-      k_records<<<grid_for(nw, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, pb, np, cb, ce, nrw.p,
-                                                              ow.p, nw, wrecs.p, wgt.p);
-      TL_CUDA(cudaGetLastError());
-      cub_call(s, [&](void* t, size_t& bytes) { return cub::DeviceScan::ExclusiveSum(t, bytes, wgt.p, nw + 1, s); });
-      uint64_t total = 0;
-      TL_CUDA(cudaMemcpyAsync(&total, wgt.p + nw, 8, cudaMemcpyDeviceToHost, s));
-      TL_CUDA(cudaStreamSynchronize(s));
-      G = total ? (total - 1) / T + 1 : 0;
-      tasks.alloc(std::max<uint64_t>(G, 1), s);
-      if (G) k_tasks<<<grid_for(G, 256, 148u * 32u), 256, 0, s>>>(wgt.p, uint32_t(nw), G, T, tasks.p);
-      TL_CUDA(cudaGetLastError());
-      r.launches += 1 + 2 + (G ? 1 : 0);
-    }
-    if (nc) {
-      crecs.alloc(nc, s);
-      k_records<<<grid_for(nc, 256, 148u * 32u), 256, 0, s>>>(CP.p, claim_off, og.off.p, pb, np, cb, ce, nrc.p,
-                                                              oc.p, nc, crecs.p, nullptr);
-      TL_CUDA(cudaGetLastError());
       ++r.launches;
     }
+    c[0] = hs[0];
+    c[1] = hs[1];
+    c[2] = hs[2];
+    c[3] = hs[3];
+    c[4] = hs[6];  // table_builds: sum of deg+ over the attributed pivots (m for the whole graph)
+    if (logical_from_cost) {
+      c[5] = fwd ? og.cost[1] : og.cost[2];
+      c[6] = 1;
+    }
+    TL_CUDA(cudaMemcpyAsync(&c[7], CP.p + c[0], 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaMemcpyAsync(&c[8], CP.p + c[1], 8, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+    if (cache) {
+      cutp = &og.cuts.emplace(cut_key, c).first->second;
+    } else {
+      cut_local = c;
+      cutp = &cut_local;
+    }
   }
+  std::array<uint64_t, 9>& cut = *cutp;
+  const uint64_t ccb = cut[0], cce = cut[1];
+  const uint32_t cpb = uint32_t(cut[2]), cpe = uint32_t(cut[3]);
+  r.table_builds = cut[4];
+  const bool need_logical = cut[6] == 0;
+  if (need_logical && ccb < cce) {
+    k_logical<<<grid_for(cce - ccb, 256, 148u * 32u), 256, 0, s>>>(cs, og.off.p, ccb, cce, skip_negative,
+                                                                   acc.p + kLogical);
+    TL_CUDA(cudaGetLastError());
+    ++r.launches;
+  }
+  mark("cut");
+
+  // ---- work records over [cb, ce): the whole graph when interleaving
+  const uint64_t cb = interleave ? 0 : ccb, ce = interleave ? m : cce;
+  const uint32_t pb = interleave ? 0 : cpb, pe = interleave ? og.n : cpe;
+  const uint64_t wsum = interleave ? og.cp_total : cut[8] - cut[7];  // window lengths over [cb, ce)
+  // adaptive task size: ~64 warp tasks per resident warp (per part).  A
+  // part's work must not depend on the mode: listing sizes its buffer by a
+  // counting pass over the same part (and the ranks of one job may run
+  // different modes), so a partitioned run sizes tasks for the count
+  // kernel's residency in every mode.
+  int warps = resident_warps<AotMode::count>();
+  if (nparts == 1) {
+    switch (mode) {
+      case AotMode::count: break;
+      case AotMode::hash: warps = resident_warps<AotMode::hash>(); break;
+      case AotMode::list: warps = resident_warps<AotMode::list>(); break;
+    }
+  }
+  const uint64_t work = wsum + kKappa * (ce - cb);
+  const uint64_t T =
+      std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
+  const bool long_lists = ce > cb && wsum / (ce - cb) >= TL_LONG_WINDOW;
+  mark("task size");
+
+  std::shared_ptr<AotPlan> plan;
+  const auto plan_key = std::make_tuple(cp_key, cb, ce, T);
+  if (cache) {
+    auto it = og.plans.find(plan_key);
+    if (it != og.plans.end()) plan = it->second;
+  }
+  const bool debug_paths = getenv("TL_DEBUG_PATHS") != nullptr;
+  if (!plan || debug_paths) {
+    plan = std::make_shared<AotPlan>();
+    // plan buffers belong to the handle's stream (they may outlive s)
+    cudaStream_t ps = cache ? og.stream : s;
+    if (ps != s) {
+      cudaEvent_t e;
+      TL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TL_CUDA(cudaEventRecord(e, s));
+      TL_CUDA(cudaStreamWaitEvent(ps, e, 0));
+      cudaEventDestroy(e);
+    }
+    build_plan(og, *plan, CP.p, claim_off, pb, pe, cb, ce, T, ps, s, debug_paths, r.launches);
+    if (cache) {
+      if (og.plans.size() >= 16) og.plans.clear();
+      og.plans[plan_key] = plan;
+    }
+  }
+  const uint64_t nw = plan->nw, nc = plan->nc, G = plan->G;
   mark("records");
   TL_CUDA(cudaEventRecord(ev[1], s));
 
@@ -1609,10 +1680,10 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   P.acc = acc.p;
   P.out = d_out;
   P.out_cap = out_cap;
-  P.recs = wrecs.p;
-  P.tasks = tasks.p;
+  P.recs = plan->wrecs.p;
+  P.tasks = plan->tasks.p;
   P.gtasks = G;
-  P.crecs = crecs.p;
+  P.crecs = plan->crecs.p;
   P.toff = interleave ? part : 0;
   P.tstride = interleave ? nparts : 1;
   P.ntasks = G > P.toff ? (G - P.toff + P.tstride - 1) / P.tstride : 0;
@@ -1645,18 +1716,19 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
   unsigned long long h[kAccN];
-  uint64_t wcb = 0, wce = 0;
   TL_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-  TL_CUDA(cudaMemcpyAsync(&wcb, CP.p + ccb, 8, cudaMemcpyDeviceToHost, s));  // this part's windows (the cut)
-  TL_CUDA(cudaMemcpyAsync(&wce, CP.p + cce, 8, cudaMemcpyDeviceToHost, s));
   TL_CUDA(cudaStreamSynchronize(s));
   TL_CUDA(cudaEventElapsedTime(&r.prep_ms, ev[0], ev[1]));
   TL_CUDA(cudaEventElapsedTime(&r.list_ms, ev[1], ev[2]));
   r.positive = h[kPos];
   r.negative = h[kNeg];
   r.executed = h[kExec];  // traversal ids loaded (after the rank-window pruning and the early exit)
-  r.windowed = CP.p ? wce - wcb : 0;
-  if (!logical_from_cost) r.logical = h[kLogical];
+  r.windowed = cut[8] - cut[7];
+  if (need_logical) {
+    cut[5] = h[kLogical];
+    cut[6] = 1;
+  }
+  r.logical = cut[5];
   r.hash_sum = h[kHsum];
   r.hash_xor = h[kHxor];
   r.emitted = h[kEmitted];

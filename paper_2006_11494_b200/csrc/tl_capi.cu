@@ -120,6 +120,7 @@ tl_oriented::~tl_oriented() {
   claim_s.reset();
   fwd_win.reset();  // every buffer is freed on its stream before the stream goes
   cp.reset();
+  plans.clear();
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

@@ -4,10 +4,16 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <array>
 #include <map>
+#include <memory>
 #include <tuple>
 
 #include "tl_common.cuh"
+
+namespace tlb {
+struct AotPlan;  // a run's work records and tasks (tl_aot.cu), cached per handle
+}
 
 // Opaque C-ABI handles (trilist_b200.h).
 struct tl_graph {
@@ -54,8 +60,16 @@ struct tl_oriented {
   // forward << 1 | skip_negative
   tlb::DBuf<uint64_t> cp;
   uint32_t cp_key = ~0u;
+  uint64_t cp_total = 0;  // CP[m]
   // emission count per (algorithm, skip_negative, part, nparts): sizes listing buffers
   std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>, uint64_t> tri_cache;
+  // Work construction cached per handle (the graph is immutable): the cost
+  // cut of a part per (claim set, part, nparts, range) -- {cb, ce, pb, pe, vb,
+  // ve, table_builds, logical, has_logical} -- and the work records + tasks per
+  // (claim set, claim range, task size).  A step of a partitioned run then
+  // rebuilds nothing.
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::array<uint64_t, 9>> cuts;
+  std::map<std::tuple<uint32_t, uint64_t, uint64_t, uint64_t>, std::shared_ptr<tlb::AotPlan>> plans;
   ~tl_oriented();
 };
 

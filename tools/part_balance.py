@@ -37,18 +37,21 @@ def main():
     run = og.count if a.mode == "count" else og.hash
     whole = min(run()["list_ms"] for _ in range(a.reps))
     for n in map(int, a.nparts.split(",")):
-        times, tri = [], 0
+        times, tri, prep_first, prep_cached = [], 0, [], []
         for p in range(n):
             best = None
-            for _ in range(a.reps):
+            for i in range(a.reps):
                 st = run(part=p, nparts=n)
                 best = st["list_ms"] if best is None else min(best, st["list_ms"])
+                (prep_first if i == 0 else prep_cached).append(st["prep_ms"])
             times.append(best)
             tri += st["triangles"]
         print(json.dumps({"config": a.config, "mode": a.mode, "nparts": n, "whole_ms": round(whole, 3),
                           "part_ms": [round(t, 3) for t in times], "max_ms": round(max(times), 3),
                           "mean_ms": round(sum(times) / n, 3), "balance": round(sum(times) / n / max(times), 4),
-                          "ideal_speedup": round(whole / max(times), 3), "triangles_sum": tri}), flush=True)
+                          "ideal_speedup": round(whole / max(times), 3), "triangles_sum": tri,
+                          "prep_ms_first_call_max": round(max(prep_first), 3),
+                          "prep_ms_cached_max": round(max(prep_cached), 3) if prep_cached else None}), flush=True)
 
 
 if __name__ == "__main__":
