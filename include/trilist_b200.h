@@ -236,6 +236,32 @@ TL_API int tl_verify(tl_oriented* og, const uint32_t* algorithms, uint32_t nalgo
                      const uint32_t* reference, uint64_t nreference, int have_reference,
                      tl_verify_result* results, uint64_t* reference_count);
 
+/* ------------------------------------------- several GPUs, one process */
+/* run_parallel_* over a device list (parallel.hpp:25-88; ParallelConfig,
+ * parallel.hpp:14-17, is the reference's only knob).  tl_multi_create
+ * replicates the oriented graph on devs[0..ndev) (device-to-device copies of
+ * the resident CSR + claims; a device equal to og's own uses og itself,
+ * borrowed: og must outlive the tl_multi) and creates one NCCL communicator
+ * per device (ncclCommInitAll; NCCL is loaded at run time).  A run splits the
+ * directed edges into ndev cost-balanced parts (part d on devs[d], one host
+ * thread per device, no exchange during compute); the counters and the hash
+ * sum are combined by ncclAllReduce(sum), the hash xors and the per-device
+ * emission counts by ncclAllGather, folded as tl_fold_parts does.  Results are
+ * identical to the single-device calls for any ndev.  opt->part/nparts must
+ * be 0/1 and opt->stream NULL.  tl_multi_list writes part d's raw emissions at
+ * its gathered offset (triples == NULL only counts). */
+typedef struct tl_multi tl_multi;
+TL_API int tl_multi_create(tl_oriented* og, const int* devs, int ndev, tl_multi** out);
+TL_API int tl_multi_free(tl_multi* mg);
+TL_API int tl_multi_count(tl_multi* mg, const tl_run_options* opt, tl_stats* stats);
+TL_API int tl_multi_hash(tl_multi* mg, const tl_run_options* opt, tl_stats* stats);
+TL_API int tl_multi_list(tl_multi* mg, const tl_run_options* opt, uint32_t* triples, uint64_t cap, tl_stats* stats);
+/* Host fold of per-part stats (any multi-GPU caller, e.g. torch.distributed
+ * ranks that gathered their tl_stats): counters and hash_sum summed mod 2^64,
+ * hash_xor xor-ed, list_ms / prep_ms = the slowest part's, offsets[d] (may be
+ * NULL) = exclusive scan of the parts' triangle counts (listing offsets). */
+TL_API int tl_fold_parts(const tl_stats* parts, uint32_t nparts, tl_stats* total, uint64_t* offsets);
+
 /* degeneracy_order / random_order -- ordering.cpp:86-120.  The degeneracy
  * order removes, one vertex at a time, the vertex of least (current degree,
  * id) -- an inherently sequential chain -- and random_order is a Fisher-Yates

@@ -198,6 +198,9 @@ class OrientedGraph {
 
   tl_oriented* handle() const { return h_.get(); }
   int device() const { return device_; }
+  /// Extension: this graph replicated on `devices` (created on first use and
+  /// kept; tl_multi_create), for runs split over several GPUs.
+  tl_multi* multi(const std::vector<int>& devices) const;
 
  private:
   friend OrientedGraph orient(const Graph&, const VertexOrder&);
@@ -218,6 +221,8 @@ class OrientedGraph {
   VertexId max_out_ = 0;
   LocalOrder local_;
   mutable std::shared_ptr<HostLayout> host_;
+  mutable std::shared_ptr<tl_multi> multi_;
+  mutable std::vector<int> multi_devices_;
 };
 
 OrientedGraph orient(const Graph& g, const VertexOrder& order);
@@ -462,11 +467,19 @@ VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algor
 struct ParallelConfig {
   unsigned workers = 1;
   VertexId chunk = 64;
+  /// Extension: the CUDA devices run_parallel_count / run_parallel_hashing
+  /// split the run over (tl_multi_*: replicas + NCCL).  Empty: the
+  /// TRILIST_DEVICES environment variable ("0,1,2,3") when set -- so unchanged
+  /// reference callers can use every GPU -- else the graph's own device.
+  std::vector<int> devices = {};
 };
 
 namespace detail {
 void validate(const ParallelConfig& cfg);
 }
+
+RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                            const RunOptions& opt = {});
 
 /// run_parallel (parallel.hpp:25-78): one device run; one sink per worker
 /// from the factory (:32-35).  NullSinks count; other sinks receive the
@@ -483,14 +496,18 @@ RunStats run_parallel(Algorithm algo, const OrientedGraph& g, const ParallelConf
   sinks.reserve(cfg.workers);
   for (unsigned w = 0; w < cfg.workers; ++w) sinks.push_back(make_sink(w));
   if constexpr (std::is_same_v<Sink, NullSink>) {
-    return detail::device_count(algo, g, opt, 0);
+    return run_parallel_count(algo, g, cfg, opt);
   } else {
     return detail::replay_batches(algo, g, sinks, opt);
   }
 }
 
-RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
-                            const RunOptions& opt = {});
+/// Extension: count + order-independent triangle hash, split like run_parallel_count.
+RunStats run_parallel_hashing(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                              const RunOptions& opt = {});
+namespace detail {
+std::vector<int> devices_for(const ParallelConfig& cfg, const OrientedGraph& g);  // cfg.devices / TRILIST_DEVICES
+}
 RunStats run_parallel_collecting(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
                                  std::vector<std::vector<std::array<VertexId, 3>>>& buffers,
                                  const RunOptions& opt = {});

@@ -26,7 +26,7 @@ LIB = os.path.join(LIBDIR, "libtrilist_b200.so")
 EXT = os.path.join(PKG, "trilist", "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 CLI = os.path.join(PKG, "bin", "trilist")
 
-CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_verify.cu", "tl_stream.cu", "tl_capi.cu"]
+CU_SOURCES = ["tl_build.cu", "tl_aot.cu", "tl_parse.cu", "tl_orders.cu", "tl_verify.cu", "tl_stream.cu", "tl_multi.cu", "tl_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -70,7 +70,7 @@ def build_lib(verbose: bool = False, force: bool = False) -> str:
             raise subprocess.CalledProcessError(p.returncode, cmd)
     if force or procs or _stale(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs +
-             ["-Xlinker", "--exclude-libs,ALL", "-lz"], verbose)
+             ["-Xlinker", "--exclude-libs,ALL", "-lz", "-ldl"], verbose)
     return LIB
 
 
@@ -137,7 +137,7 @@ def build_variant(name: str, verbose: bool = False, force: bool = False) -> str:
         _run([NVCC] + NVCC_FLAGS + ["-D" + d for d in VARIANTS[name]] + ["-c", src, "-o", o], verbose)
         objs = [os.path.join(OBJ, f.replace(".cu", ".o")) for f in CU_SOURCES if f != "tl_aot.cu"]
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out, o] + objs +
-             ["-Xlinker", "--exclude-libs,ALL", "-lz"], verbose)
+             ["-Xlinker", "--exclude-libs,ALL", "-lz", "-ldl"], verbose)
     return out
 
 

@@ -30,7 +30,8 @@ EXPORTS = (
     "tl_graph_from_text", "tl_graph_from_file", "tl_degree_order", "tl_orient", "tl_oriented_from_csr", "tl_oriented_free", "tl_oriented_info",
     "tl_oriented_csr", "tl_cost_model", "tl_aot_count", "tl_aot_hash", "tl_aot_list",
     "tl_run_count", "tl_run_hash", "tl_run_list", "tl_run_list_device", "tl_run_list_batches", "tl_verify", "tl_degeneracy_order", "tl_random_order",
-    "tl_brute_force",
+    "tl_brute_force", "tl_multi_create", "tl_multi_free", "tl_multi_count", "tl_multi_hash", "tl_multi_list",
+    "tl_fold_parts",
 )
 
 # TL_ALGO_* (Algorithm, engine.hpp:18) by the reference's names (engine.cpp:7-15).
@@ -142,6 +143,12 @@ def lib() -> C.CDLL:
     L.tl_degeneracy_order.argtypes = [vp, u32p]
     L.tl_random_order.argtypes = [C.c_uint32, C.c_uint64, u32p]
     L.tl_brute_force.argtypes = [vp, C.c_uint32, u32p, C.c_uint64, u64p]
+    L.tl_multi_create.argtypes = [vp, C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+    L.tl_multi_free.argtypes = [vp]
+    L.tl_multi_count.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
+    L.tl_multi_hash.argtypes = [vp, C.POINTER(TlRunOptions), C.POINTER(TlStats)]
+    L.tl_multi_list.argtypes = [vp, C.POINTER(TlRunOptions), u32p, C.c_uint64, C.POINTER(TlStats)]
+    L.tl_fold_parts.argtypes = [C.POINTER(TlStats), C.c_uint32, C.POINTER(TlStats), u64p]
     return L
 
 
@@ -423,3 +430,59 @@ class DeviceOriented:
         _check(lib().tl_run_list_device(self._h, C.byref(o), C.c_void_p(d_triples), cap, int(canonical),
                                         C.byref(st)))
         return st.as_dict()
+
+
+def fold_parts(parts) -> tuple[dict, list]:
+    """tl_fold_parts: combine per-part stats dicts (sums mod 2^64, xor, the
+    slowest part's times) -> (total dict, listing offsets)."""
+    arr = (TlStats * max(len(parts), 1))()
+    for i, p in enumerate(parts):
+        for name, _ in TlStats._fields_:
+            if name in p:
+                setattr(arr[i], name, p[name])
+    out = TlStats()
+    offs = np.zeros(max(len(parts), 1), np.uint64)
+    _check(lib().tl_fold_parts(arr, len(parts), C.byref(out), _p64(offs)))
+    return out.as_dict(), [int(x) for x in offs[: len(parts)]]
+
+
+class MultiOriented:
+    """tl_multi: the oriented graph replicated on a device list (one process),
+    each run split over the devices, results combined by NCCL."""
+
+    def __init__(self, oriented: "DeviceOriented", devices):
+        self._h = vp()
+        devs = (C.c_int * len(devices))(*devices)
+        _check(lib().tl_multi_create(oriented._h, devs, len(devices), C.byref(self._h)))
+        self._keep = oriented  # borrowed by the replica on its own device
+
+    def close(self):
+        if self._h:
+            lib().tl_multi_free(self._h)
+            self._h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def count(self, algo="aot", skip_negative=False) -> dict:
+        st = TlStats()
+        o = run_options(skip_negative, 0, 1, 0, algo)
+        _check(lib().tl_multi_count(self._h, C.byref(o), C.byref(st)))
+        return st.as_dict()
+
+    def hash(self, algo="aot", skip_negative=False) -> dict:
+        st = TlStats()
+        o = run_options(skip_negative, 0, 1, 0, algo)
+        _check(lib().tl_multi_hash(self._h, C.byref(o), C.byref(st)))
+        return st.as_dict()
+
+    def list(self, algo="aot", skip_negative=False):
+        st = TlStats()
+        o = run_options(skip_negative, 0, 1, 0, algo)
+        _check(lib().tl_multi_list(self._h, C.byref(o), None, 0, C.byref(st)))
+        out = np.empty((max(st.triangles, 1), 3), np.uint32)
+        _check(lib().tl_multi_list(self._h, C.byref(o), _p32(out), st.triangles, C.byref(st)))
+        return st.as_dict(), out[: st.triangles]

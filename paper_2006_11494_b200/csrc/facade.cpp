@@ -668,10 +668,73 @@ VerifyReport verify_equivalence(const Graph& g, std::span<const Algorithm> algor
 }
 
 // ---------------------------------------------------------------- parallel
+std::vector<int> detail::devices_for(const ParallelConfig& cfg, const OrientedGraph& g) {
+  std::vector<int> devs = cfg.devices;
+  if (devs.empty()) {
+    if (const char* e = std::getenv("TRILIST_DEVICES")) {
+      std::string text(e);
+      std::size_t i = 0;
+      while (i < text.size()) {
+        std::size_t j = text.find(',', i);
+        if (j == std::string::npos) j = text.size();
+        const std::string item = text.substr(i, j - i);
+        if (!item.empty()) {
+          int d = 0;
+          const auto r = std::from_chars(item.data(), item.data() + item.size(), d);
+          if (r.ec != std::errc() || r.ptr != item.data() + item.size())
+            throw std::invalid_argument("TRILIST_DEVICES must be a comma-separated device list, got '" + text + "'");
+          devs.push_back(d);
+        }
+        i = j + 1;
+      }
+    }
+  }
+  (void)g;
+  return devs;
+}
+
+tl_multi* OrientedGraph::multi(const std::vector<int>& devices) const {
+  if (!h_) return nullptr;
+  if (!multi_ || multi_devices_ != devices) {
+    multi_.reset();
+    tl_multi* m = nullptr;
+    check(tl_multi_create(h_.get(), devices.data(), int(devices.size()), &m), "tl_multi_create");
+    multi_ = std::shared_ptr<tl_multi>(m, [](tl_multi* p) { tl_multi_free(p); });
+    multi_devices_ = devices;
+  }
+  return multi_.get();
+}
+
+namespace {
+RunStats multi_run(Algorithm algo, const OrientedGraph& g, const std::vector<int>& devs, const RunOptions& opt,
+                   bool hashing) {
+  detail::require_device_algorithm(algo);
+  detail::assert_layout(algo, g);
+  if (!g.handle()) return RunStats{};
+  tl_run_options o = detail::options_for(algo, opt);
+  tl_stats s;
+  tl_multi* m = g.multi(devs);
+  check(hashing ? tl_multi_hash(m, &o, &s) : tl_multi_count(m, &o, &s), "multi-device run");
+  RunStats r = detail::to_run_stats(s);
+  detail::relayout_table_builds(g, opt, algo, r);
+  return r;
+}
+}  // namespace
+
 RunStats run_parallel_count(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
                             const RunOptions& opt) {
   detail::validate(cfg);
+  const std::vector<int> devs = detail::devices_for(cfg, g);
+  if (!devs.empty()) return multi_run(algo, g, devs, opt, false);
   return run_counting(algo, g, opt);
+}
+
+RunStats run_parallel_hashing(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,
+                              const RunOptions& opt) {
+  detail::validate(cfg);
+  const std::vector<int> devs = detail::devices_for(cfg, g);
+  if (!devs.empty()) return multi_run(algo, g, devs, opt, true);
+  return run_hashing(algo, g, opt);
 }
 
 RunStats run_parallel_collecting(Algorithm algo, const OrientedGraph& g, const ParallelConfig& cfg,

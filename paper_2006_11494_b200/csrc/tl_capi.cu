@@ -60,6 +60,8 @@ tl_run_options defaults() {
 
 namespace tlb {
 
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
 void fill_stats_from(const AotResult& r, tl_stats* st) {
   if (!st) return;
   std::memset(st, 0, sizeof(*st));

@@ -168,6 +168,8 @@ struct RunSpec {
 // out/out_cap only for AotMode::list (device buffer of 3*out_cap uint32).
 AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t* d_out, uint64_t out_cap);
 void fill_stats_from(const AotResult& r, tl_stats* st);  // tl_capi.cu
+void ensure_device_setup(int device);                     // tl_capi.cu
+void set_last_error(const std::string& msg);              // tl_capi.cu: the thread's tl_last_error()
 
 // ---- tl_stream.cu ----
 // Batched listing (tl_run_list_batches): emissions of `spec` in batches of at

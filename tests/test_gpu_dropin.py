@@ -42,6 +42,17 @@ def test_reference_acceptance_gate_unchanged():
     assert p.returncode == 0 and "all acceptance criteria passed" in p.stdout
 
 
+def test_reference_acceptance_gate_over_the_device_list():
+    """The same unchanged binary with TRILIST_DEVICES set: every
+    run_parallel_count (criteria 5 and 8) goes through tl_multi_* -- replicas,
+    one host thread per device, NCCL all-reduce / all-gather of the results."""
+    _need(ACCEPTANCE)
+    env = dict(os.environ, TRILIST_DEVICES="0", NCCL_DEBUG="WARN")
+    p = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=600, env=env)
+    print(p.stdout)
+    assert p.returncode == 0 and "all acceptance criteria passed" in p.stdout, p.stdout + p.stderr
+
+
 def test_reference_python_smoke_unchanged():
     _need(SMOKE)
     env = dict(os.environ, PYTHONPATH=os.path.join(DROPIN, "python"))

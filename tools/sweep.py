@@ -34,7 +34,7 @@ def build(specs):
         assert p.wait() == 0, name
         lib = os.path.join(VDIR, f"lib_{name}.so")
         subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib, o] + objs +
-                       ["-Xlinker", "--exclude-libs,ALL", "-lz"], check=True)
+                       ["-Xlinker", "--exclude-libs,ALL", "-lz", "-ldl"], check=True)
         print("built", lib)
 
 
