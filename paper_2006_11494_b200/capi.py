@@ -452,6 +452,7 @@ class MultiOriented:
 
     def __init__(self, oriented: "DeviceOriented", devices):
         self._h = vp()
+        import torch  # noqa: F401 -- loads PyTorch's NCCL first; tl_multi then shares it
         devs = (C.c_int * len(devices))(*devices)
         _check(lib().tl_multi_create(oriented._h, devs, len(devices), C.byref(self._h)))
         self._keep = oriented  # borrowed by the replica on its own device

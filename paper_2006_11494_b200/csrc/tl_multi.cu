@@ -12,9 +12,9 @@
 //   * ncclAllGather of the per-device hash xor (NCCL has no XOR) and of the
 //     per-device emission counts (-> each device's listing offset),
 // folded by tl_fold_parts, the same host function a torch.distributed caller
-// uses.  NCCL is loaded at run time (dlopen "libnccl.so.2"): the library has
-// no link-time NCCL dependency, and a process that already loaded NCCL
-// (PyTorch) shares that copy.
+// uses.  NCCL is loaded at run time (dlopen): the library has no link-time
+// NCCL dependency, and a process that already loaded NCCL (PyTorch) shares
+// that copy -- a process that loads PyTorch should import it first.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -33,7 +33,8 @@ struct tl_multi {
   std::vector<tl_oriented*> reps;  // reps[d] on devs[d]
   std::vector<bool> owned;         // false: the caller's handle, borrowed
   std::vector<ncclComm_t> comms;
-  std::vector<tlb::DBuf<unsigned long long>> red;  // per device: 8 sums + ndev xors + ndev counts
+  std::vector<cudaStream_t> streams;               // per device: the collectives' own streams
+  std::vector<tlb::DBuf<unsigned long long>> red;  // per device (on streams[d]): 8 sums + ndev xors + ndev counts
   ~tl_multi();
 };
 
@@ -55,8 +56,14 @@ const Nccl& nccl() {
   static Nccl n;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // an NCCL the process already loaded (PyTorch's) first, then TL_NCCL_LIB,
+    // then the system library -- loading a second copy of libnccl.so.2 first
+    // would shadow a framework's newer one
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)
+      if (const char* path = getenv("TL_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       n.load_error = std::string("NCCL not available: ") + dlerror();
       return;
@@ -166,11 +173,11 @@ void reduce_parts(tl_multi& mg, const std::vector<AotResult>& parts, tl_stats* o
     to_sums(parts[d], h.data());
     h[kNSums + d] = parts[d].hash_xor;       // gathered into slot d
     h[kNSums + nd + d] = parts[d].emitted ? parts[d].emitted : parts[d].triangles;
-    TL_CUDA(cudaMemcpyAsync(mg.red[d].p, h.data(), words * 8, cudaMemcpyHostToDevice, mg.reps[d]->stream));
+    TL_CUDA(cudaMemcpyAsync(mg.red[d].p, h.data(), words * 8, cudaMemcpyHostToDevice, mg.streams[d]));
   }
   nccl_check(N.group_start(), "ncclGroupStart");
   for (int d = 0; d < nd; ++d) {
-    cudaStream_t st = mg.reps[d]->stream;
+    cudaStream_t st = mg.streams[d];
     unsigned long long* b = mg.red[d].p;
     nccl_check(N.all_reduce(b, b, kNSums, ncclUint64, ncclSum, mg.comms[d], st), "ncclAllReduce");
     nccl_check(N.all_gather(b + kNSums + d, b + kNSums, 1, ncclUint64, mg.comms[d], st), "ncclAllGather(xor)");
@@ -181,12 +188,12 @@ void reduce_parts(tl_multi& mg, const std::vector<AotResult>& parts, tl_stats* o
   std::vector<unsigned long long> h(words);
   {
     DeviceGuard guard(mg.devs[0]);
-    TL_CUDA(cudaMemcpyAsync(h.data(), mg.red[0].p, words * 8, cudaMemcpyDeviceToHost, mg.reps[0]->stream));
-    TL_CUDA(cudaStreamSynchronize(mg.reps[0]->stream));
+    TL_CUDA(cudaMemcpyAsync(h.data(), mg.red[0].p, words * 8, cudaMemcpyDeviceToHost, mg.streams[0]));
+    TL_CUDA(cudaStreamSynchronize(mg.streams[0]));
   }
   for (int d = 1; d < nd; ++d) {
     DeviceGuard guard(mg.devs[d]);
-    TL_CUDA(cudaStreamSynchronize(mg.reps[d]->stream));
+    TL_CUDA(cudaStreamSynchronize(mg.streams[d]));
   }
   // per-part stats as the devices reported them, the collective's sums checked against the host fold
   std::vector<tl_stats> ps(nd);
@@ -213,10 +220,16 @@ tl_multi::~tl_multi() {
   if (!comms.empty() && tlb::nccl().comm_destroy)
     for (auto c : comms)
       if (c) tlb::nccl().comm_destroy(c);
-  for (size_t d = 0; d < reps.size(); ++d) {
+  // never touches a borrowed handle: it may already be gone (garbage collectors
+  // do not order finalizers)
+  for (size_t d = 0; d < devs.size(); ++d) {
     tlb::DeviceGuard guard(devs[d]);
-    red[d].reset();
-    if (owned[d]) delete reps[d];
+    if (d < red.size()) red[d].reset();
+    if (d < streams.size() && streams[d]) {
+      cudaStreamSynchronize(streams[d]);
+      cudaStreamDestroy(streams[d]);
+    }
+    if (d < reps.size() && owned[d]) delete reps[d];
   }
 }
 
@@ -314,9 +327,12 @@ int tl_multi_create(tl_oriented* og, const int* devs, int ndev, tl_multi** out) 
       const bool same = devs[d] == og->device;
       mg->reps.push_back(same ? og : tlb::replicate(*og, devs[d]));
       mg->owned.push_back(!same);
-      mg->red.emplace_back();
       tlb::DeviceGuard guard(devs[d]);
-      mg->red.back().alloc(8 + 2 * size_t(ndev), mg->reps.back()->stream);
+      cudaStream_t st = nullptr;
+      TL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      mg->streams.push_back(st);
+      mg->red.emplace_back();
+      mg->red.back().alloc(8 + 2 * size_t(ndev), st);
     }
     mg->comms.assign(ndev, nullptr);
     tlb::nccl_check(N.comm_init_all(mg->comms.data(), ndev, devs), "ncclCommInitAll");
