@@ -6,15 +6,15 @@
 // through trilist::run_parallel over the B200 facade, which streams the
 // emissions from the device in bounded host batches.  Prints one JSON line:
 // the triangle hash (count, sum, xor), the counters, the wall time and the
-// process's peak resident set (getrusage), so a test can check both the
+// process's peak resident set (VmHWM), so a test can check both the
 // result (against the reference's golden hash) and the bounded host memory.
 //
 //   stream_sink_check <er|rmat|chung_lu> <seed> <n or scale> <npairs> [workers] [avg gamma]
 #include <cuda_runtime.h>
-#include <sys/resource.h>
 
 #include <chrono>
 #include <cstdio>
+#include <fstream>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -107,8 +107,20 @@ int main(int argc, char** argv) {
     x ^= a.v[2];
     busy += a.v[0] != 0;
   }
-  rusage ru{};
-  getrusage(RUSAGE_SELF, &ru);
+  // Peak resident set of THIS program: VmHWM (reset at exec), not
+  // getrusage's ru_maxrss, which Linux carries over from the pre-exec image
+  // of a forked parent (a large test runner would show up as ours).
+  long hwm_kb = -1;
+  {
+    std::ifstream status("/proc/self/status");
+    std::string line;
+    while (std::getline(status, line)) {
+      if (line.rfind("VmHWM:", 0) == 0) hwm_kb = std::strtol(line.c_str() + 6, nullptr, 10);
+      if (line.rfind("VmHWM", 0) == 0 || line.rfind("VmRSS", 0) == 0 || line.rfind("RssAnon", 0) == 0 ||
+          line.rfind("RssFile", 0) == 0 || line.rfind("RssShmem", 0) == 0)
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
+  }
   std::printf(
       "{\"n\": %u, \"m\": %llu, \"hash_count\": %llu, \"hash_sum\": %llu, \"hash_xor\": %llu, \"triangles\": %llu, "
       "\"probes\": %llu, \"table_builds\": %llu, \"positive_triangles\": %llu, \"negative_triangles\": %llu, "
@@ -117,6 +129,6 @@ int main(int argc, char** argv) {
       (unsigned long long)x, (unsigned long long)s.triangles, (unsigned long long)s.probes,
       (unsigned long long)s.table_builds, (unsigned long long)s.positive_triangles,
       (unsigned long long)s.negative_triangles, workers, (unsigned long long)busy, wall, s.wall_time_s,
-      ru.ru_maxrss);
+      hwm_kb);
   return 0;
 }
