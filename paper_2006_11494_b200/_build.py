@@ -121,6 +121,9 @@ VARIANTS = {
                    "TL_CTA_HASH_DEG=16", "TL_BUCKET_PROBE=0"],  # linear-probing hashes + global search
     "paths_fallback": ["TL_WARP_WORDS=32", "TL_CTA_MIN_WORK=1024", "TL_RANK_PROBE=0",
                        "TL_BUCKET_FORCE_FAIL=1"],  # bucket hashes that fail and fall back
+    # the in-kernel count of loaded traversal ids (off in the product build,
+    # which computes probes_executed with k_executed): the two must agree
+    "exec_count": ["TL_EXEC_COUNT=1"],
 }
 
 

@@ -264,6 +264,14 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// In-kernel count of the traversal ids loaded (TL_EXEC_COUNT=1: a shared
+// counter per warp, one add per packed batch / long list).  Off by default:
+// it cost 3.7% of the C4 count kernel (277.4 vs 270.7 ms, tools/sweep.py); the
+// same number is computed outside the hot loop by k_executed (below), which
+// replays the early-exit rule per claim.
+#ifndef TL_EXEC_COUNT
+#define TL_EXEC_COUNT 0
+#endif
 // Per-warp count of the traversal ids the kernel actually loads (probes left
 // after the rank-window pruning and the in-kernel early exit): one shared
 // 64-bit word per warp, added to by lane 0 once per packed round group / long
@@ -699,7 +707,7 @@ __device__ __forceinline__ void ring_sweep(const Params& P, const Probe& probe, 
     s = s + 1 == kRingStages ? 0u : s + 1;
     if (++cc == cn) {
       if (cneg) st.neg += hits; else st.pos += hits;
-      if (lane == 0) red_add_sm64(exec_addr(), cl);
+      if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), cl);
       cm &= cm - 1;
       if (!cm) break;
       cj = __ffs(cm) - 1;
@@ -746,7 +754,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   const uint32_t excl = incl - slen;
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   const uint64_t bm = b - excl;  // element q of the packed stream: col[bm(owner) + q]
-  if (lane == 0 && total) red_add_sm64(exec_addr(), total);
+  if (TL_EXEC_COUNT && lane == 0 && total) red_add_sm64(exec_addr(), total);
 #ifndef TL_SHORT_UNROLL
 #define TL_SHORT_UNROLL 4
 #endif
@@ -826,7 +834,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       if (__any_sync(kFull, over)) break;
     }
     if (nj) st.neg += hits; else st.pos += hits;
-    if (lane == 0) red_add_sm64(exec_addr(), min(lj, uint32_t(int(lj) - rem)));  // ids loaded before the exit
+    if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), min(lj, uint32_t(int(lj) - rem)));  // ids loaded
   }
 }
 
@@ -842,9 +850,11 @@ __device__ __forceinline__ void reduce_and_flush(Lane<MODE>& st, const Params& P
     v[3] ^= __shfl_xor_sync(kFull, v[3], o);
   }
   if (lane_id() == 0) {
-    const unsigned long long ex = *reinterpret_cast<volatile unsigned long long*>(
-        __cvta_shared_to_generic(exec_addr()));
-    if (ex) atomicAdd(P.acc + kExec, ex);
+    if constexpr (TL_EXEC_COUNT) {
+      const unsigned long long ex =
+          *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr()));
+      if (ex) atomicAdd(P.acc + kExec, ex);
+    }
     if (v[0]) atomicAdd(P.acc + kPos, v[0]);
     if (v[1]) atomicAdd(P.acc + kNeg, v[1]);
     if (v[2]) atomicAdd(P.acc + kHsum, v[2]);
@@ -1006,7 +1016,8 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t wbase = sm_addr(warp * kWarpStride);
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
-  if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr())) = 0ull;
+  if constexpr (TL_EXEC_COUNT)
+    if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr())) = 0ull;
   Lane<MODE> st;
   st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (2 * emit_cap<MODE>()));
   if constexpr (ring_mode<MODE>()) {
@@ -1126,6 +1137,47 @@ __global__ void k_logical(const uint32_t* cs, const uint64_t* off, uint64_t cb, 
   }
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
+}
+
+// Traversal ids the kernel loads for the claims [cb, ce) of pivots [pb, pe)
+// (probes_executed), by the rule of claim_batch's register path: a window of
+// at most kShort ids is loaded whole (packed rounds); a longer one in groups
+// of G = 32U ids, group g being loaded iff no earlier group held an id above
+// max N+(l) (lists ascend), i.e. min(len, G * (g* + 1)) ids, g* = the group
+// of the first id above max N+(l).  One warp per pivot, a binary search per
+// long claim; run once per cut and cached.
+__global__ void k_executed(const uint64_t* claim_off, const uint64_t* off, const uint32_t* col, const uint64_t* win,
+                           uint32_t pb, uint32_t pe, uint64_t cb, uint64_t ce, uint32_t G, uint32_t skip_neg,
+                           unsigned long long* acc) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long sum = 0;
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < uint64_t(pe - pb); w += nwarps) {
+    const uint32_t l = pb + uint32_t(w);
+    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
+    if (a >= b) continue;
+    const uint64_t lb = off[l], le = off[l + 1];
+    if (lb == le) continue;
+    const uint32_t lmax = __ldg(col + le - 1);
+    for (uint64_t c = a + lane; c < b; c += 32) {
+      const uint64_t wv = win[c];
+      if (skip_neg && (wv >> 63)) continue;
+      const uint64_t s = wv & kWinBeginMask;
+      const uint32_t len = uint32_t((wv >> kWinLenShift) & kWinLenMask);
+      if (len <= kShort) {
+        sum += len;
+        continue;
+      }
+      uint32_t lo = 0, hi = len;  // first position with an id above lmax
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(col + s + mid) <= lmax) lo = mid + 1; else hi = mid;
+      }
+      sum += lo == len ? len : min(len, G * (lo / G + 1));
+    }
+  }
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+  if (lane == 0 && sum) atomicAdd(acc, sum);
 }
 
 // Warp path: the span fits the warp bitmap, or a small pivot (warp hash) with
@@ -1566,16 +1618,17 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   const bool interleave = !whole && !spec.range && !(split_mode && std::string(split_mode) == "range") &&
                           spec.algo != Algo::cf_merge;
   const bool cache = !spec.range;  // batched listing walks thousands of ranges once each
-  // ---- the part's cost cut: {cb, ce, pb, pe, table_builds, logical, has_logical, CP[cb], CP[ce]}
-  std::array<uint64_t, 9> cut_local{};
-  std::array<uint64_t, 9>* cutp = nullptr;
+  // ---- the part's cost cut: {cb, ce, pb, pe, table_builds, logical, has_logical, CP[cb], CP[ce],
+  //      executed, group size the executed count was made for (0: none)}
+  std::array<uint64_t, 11> cut_local{};
+  std::array<uint64_t, 11>* cutp = nullptr;
   const auto cut_key = std::make_tuple(cp_key, whole ? 0u : part, whole ? 1u : nparts);
   if (cache) {
     auto it = og.cuts.find(cut_key);
     if (it != og.cuts.end()) cutp = &it->second;
   }
   if (!cutp) {
-    std::array<uint64_t, 9> c{};
+    std::array<uint64_t, 11> c{};
     uint64_t hs[8] = {0, m, 0, og.n, 0, 0, m, 0};
     DBuf<uint64_t> split;
     split.alloc(8, s);
@@ -1605,7 +1658,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
       cutp = &cut_local;
     }
   }
-  std::array<uint64_t, 9>& cut = *cutp;
+  std::array<uint64_t, 11>& cut = *cutp;
   const uint64_t ccb = cut[0], cce = cut[1];
   const uint32_t cpb = uint32_t(cut[2]), cpe = uint32_t(cut[3]);
   r.table_builds = cut[4];
@@ -1639,6 +1692,15 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   const uint64_t T =
       std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
   const bool long_lists = ce > cb && wsum / (ce - cb) >= TL_LONG_WINDOW;
+  // probes_executed of the cut's claims under this run's group size (once per cut)
+  uint32_t group = 32u * uint32_t(long_lists ? (mode == AotMode::count ? kUnrollLong : kUnrollLongEmit) : kUnrollShort);
+  const bool need_executed = !TL_EXEC_COUNT && cut[10] != group;
+  if (need_executed && ccb < cce) {
+    k_executed<<<grid_for(uint64_t(cpe - cpb) * 32, 256, 148u * 64u), 256, 0, s>>>(
+        claim_off, og.off.p, og.col.p, cwin, cpb, cpe, ccb, cce, group, skip_negative, acc.p + kExec);
+    TL_CUDA(cudaGetLastError());
+    ++r.launches;
+  }
   mark("task size");
 
   std::shared_ptr<AotPlan> plan;
@@ -1722,7 +1784,12 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   TL_CUDA(cudaEventElapsedTime(&r.list_ms, ev[1], ev[2]));
   r.positive = h[kPos];
   r.negative = h[kNeg];
-  r.executed = h[kExec];  // traversal ids loaded (after the rank-window pruning and the early exit)
+  if (need_executed) {
+    cut[9] = h[kExec];
+    cut[10] = group;
+  }
+  // traversal ids loaded (after the rank-window pruning and the early exit)
+  r.executed = TL_EXEC_COUNT ? h[kExec] : cut[9];
   r.windowed = cut[8] - cut[7];
   if (need_logical) {
     cut[5] = h[kLogical];

@@ -15,6 +15,7 @@ from paper_2006_11494_b200 import trilist
 from paper_2006_11494_b200.configs import CONFIGS
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 KERNELS = ("cf", "cf-hash", "kclist", "aot")
 ORDERS = ("degree", "degeneracy", "id", "random:11")
@@ -230,3 +231,42 @@ def test_partitioned_listing_at_scale():
     golden = json.load(open(os.path.join(os.path.dirname(GOLDEN), "configs.json")))["c3"]
     assert total == golden["triangles"]
     og.close()
+
+
+_EXEC_SNIPPET = r"""
+import json, sys
+sys.path.insert(0, {root!r})
+import oracle as O
+from paper_2006_11494_b200 import capi
+pairs = O.gen_rmat(17, 13, 16 << 13)
+do = capi.DeviceGraph.from_pairs(pairs, 1 << 13).orient()
+out = {{}}
+for algo in ("aot", "cf", "cf-hash", "kclist"):
+    for mode in ("count", "hash"):
+        run = do.count if mode == "count" else do.hash
+        out[f"{{algo}}/{{mode}}"] = run(algo=algo)["probes_executed"]
+        out[f"{{algo}}/{{mode}}/skip"] = run(algo=algo, skip_negative=True)["probes_executed"]
+print(json.dumps(out))
+"""
+
+
+def test_probes_executed_matches_the_kernels_own_count():
+    """probes_executed (computed outside the hot loop by k_executed from the
+    early-exit rule) equals the count the kernel itself keeps when built with
+    TL_EXEC_COUNT=1 (lib/variants/lib_exec_count.so), for every kernel, mode
+    and the fault hook; and the parts of a split sum to the whole."""
+    import json
+    import subprocess
+    import sys
+
+    from paper_2006_11494_b200 import _build
+
+    lib = os.path.join(_build.LIBDIR, "variants", "lib_exec_count.so")
+    assert os.path.exists(lib), lib
+    code = _EXEC_SNIPPET.format(root=ROOT)
+    ref = json.loads(subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True,
+                                    env=dict(os.environ, TL_LIB_PATH=lib)).stdout.strip().splitlines()[-1])
+    ours = json.loads(subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                                     check=True).stdout.strip().splitlines()[-1])
+    assert ours == ref
+    assert all(v > 0 for k, v in ours.items() if not k.startswith("cf/"))
