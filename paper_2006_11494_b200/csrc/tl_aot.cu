@@ -148,6 +148,10 @@ constexpr bool kRingAsync = TL_RING == 2;  // 2: per-thread cp.async (LDGSTS); 1
 static_assert(!kRingAsync || kRingWords % 128 == 0, "LDGSTS chunks are 128-word multiples");
 static_assert((kRingWords & (kRingWords - 1)) == 0 && kRingWords >= 32 && kRingWords <= 256, "ring chunk size");
 
+#ifndef TL_FLUSH_UNROLL
+#define TL_FLUSH_UNROLL 4
+#endif
+constexpr int kFlushUnroll = TL_FLUSH_UNROLL;  // staged hits gathered in flight per lane in a flush
 // per-warp staging of hits (hash / list modes)
 template <AotMode MODE>
 constexpr int emit_cap() {
@@ -526,7 +530,7 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
         if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
         base = __shfl_sync(kFull, base, 0);
       }
-#pragma unroll 4
+#pragma unroll kFlushUnroll
       for (uint32_t i = lane_id(); i < cnt; i += 32) {
         const uint2 e = ld_sm2(st.ebase + 8 * i);
         uint32_t c = __ldg(P.orig + e.y);
@@ -1168,12 +1172,18 @@ __global__ void k_executed(const uint64_t* claim_off, const uint64_t* off, const
         sum += len;
         continue;
       }
-      uint32_t lo = 0, hi = len;  // first position with an id above lmax
+      // the windows are nearly tight: most end at or below max N+(l) and are
+      // loaded whole (one load decides); otherwise search the exit position
+      if (__ldg(col + s + len - 1) <= lmax) {
+        sum += len;
+        continue;
+      }
+      uint32_t lo = 0, hi = len - 1;  // first position with an id above lmax (the last one is)
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (__ldg(col + s + mid) <= lmax) lo = mid + 1; else hi = mid;
       }
-      sum += lo == len ? len : min(len, G * (lo / G + 1));
+      sum += min(len, G * (lo / G + 1));
     }
   }
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
@@ -1695,10 +1705,28 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   // probes_executed of the cut's claims under this run's group size (once per cut)
   uint32_t group = 32u * uint32_t(long_lists ? (mode == AotMode::count ? kUnrollLong : kUnrollLongEmit) : kUnrollShort);
   const bool need_executed = !TL_EXEC_COUNT && cut[10] != group;
+  // it runs on the handle's side stream, overlapped with the listing kernel
+  // (it is latency-bound; ~15 ms at C4 when alone), and s joins it before
+  // the counters are read back
+  cudaEvent_t exec_done = nullptr;
+  struct ExecEvGuard {
+    cudaEvent_t& e;
+    ~ExecEvGuard() {
+      if (e) cudaEventDestroy(e);
+    }
+  } exec_guard{exec_done};
   if (need_executed && ccb < cce) {
-    k_executed<<<grid_for(uint64_t(cpe - cpb) * 32, 256, 148u * 64u), 256, 0, s>>>(
+    if (!og.aux) TL_CUDA(cudaStreamCreateWithFlags(&og.aux, cudaStreamNonBlocking));
+    cudaEvent_t ready;
+    TL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(ready, s));  // acc zeroed, CP / claims ready
+    TL_CUDA(cudaStreamWaitEvent(og.aux, ready, 0));
+    cudaEventDestroy(ready);
+    k_executed<<<grid_for(uint64_t(cpe - cpb) * 32, 256, 148u * 64u), 256, 0, og.aux>>>(
         claim_off, og.off.p, og.col.p, cwin, cpb, cpe, ccb, cce, group, skip_negative, acc.p + kExec);
     TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaEventCreateWithFlags(&exec_done, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(exec_done, og.aux));
     ++r.launches;
   }
   mark("task size");
@@ -1777,6 +1805,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     }
   }
   TL_CUDA(cudaEventRecord(ev[2], s));
+  if (exec_done) TL_CUDA(cudaStreamWaitEvent(s, exec_done, 0));
   unsigned long long h[kAccN];
   TL_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
   TL_CUDA(cudaStreamSynchronize(s));

@@ -123,6 +123,10 @@ tl_oriented::~tl_oriented() {
   fwd_win.reset();  // every buffer is freed on its stream before the stream goes
   cp.reset();
   plans.clear();
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
+  }
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);

@@ -41,6 +41,7 @@ struct tl_graph {
 struct tl_oriented {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // side stream for work overlapped with a run (created on first use)
   uint32_t n = 0;
   uint32_t nb = 0;
   uint64_t m = 0;
