@@ -1143,51 +1143,52 @@ __global__ void k_logical(const uint32_t* cs, const uint64_t* off, uint64_t cb, 
   if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
 }
 
-// Traversal ids the kernel loads for the claims [cb, ce) of pivots [pb, pe)
-// (probes_executed), by the rule of claim_batch's register path: a window of
+// Traversal ids the listing kernel loads (probes_executed) for the records
+// this run executes, by the rule of claim_batch's register path: a window of
 // at most kShort ids is loaded whole (packed rounds); a longer one in groups
 // of G = 32U ids, group g being loaded iff no earlier group held an id above
-// max N+(l) (lists ascend), i.e. min(len, G * (g* + 1)) ids, g* = the group
-// of the first id above max N+(l).  One warp per pivot, a binary search per
-// long claim; run once per cut and cached.
-__global__ void k_executed(const uint64_t* claim_off, const uint64_t* off, const uint32_t* col, const uint64_t* win,
-                           uint32_t pb, uint32_t pe, uint64_t cb, uint64_t ce, uint32_t G, uint32_t skip_neg,
-                           unsigned long long* acc) {
+// max N+(l) (lists ascend): min(len, G * (g* + 1)) ids, g* = the group of the
+// first id above max N+(l).  Windows are nearly tight, so one load of the
+// window's last id settles most of them.  One warp per warp task (its records)
+// and per CTA record of this part; run once per plan and part, cached.
+__device__ __forceinline__ unsigned long long executed_of_record(const Rec& R, const uint64_t* win,
+                                                                 const uint32_t* col, uint32_t G, uint32_t skip_neg) {
   const uint32_t lane = threadIdx.x & 31;
+  unsigned long long sum = 0;
+  if (R.dl == 0) return 0;
+  const uint32_t lmax = __ldg(col + R.lb + R.dl - 1);
+  for (uint64_t c = R.cb + lane; c < R.ce; c += 32) {
+    const uint64_t wv = win[c];
+    if (skip_neg && (wv >> 63)) continue;
+    const uint64_t s = wv & kWinBeginMask;
+    const uint32_t len = uint32_t((wv >> kWinLenShift) & kWinLenMask);
+    if (len <= kShort || __ldg(col + s + len - 1) <= lmax) {
+      sum += len;
+      continue;
+    }
+    uint32_t lo = 0, hi = len - 1;  // first position with an id above lmax (the last one is)
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(col + s + mid) <= lmax) lo = mid + 1; else hi = mid;
+    }
+    sum += min(len, G * (lo / G + 1));
+  }
+  return sum;
+}
+
+__global__ void k_executed(Params P, uint32_t G, unsigned long long* out) {
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   unsigned long long sum = 0;
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < uint64_t(pe - pb); w += nwarps) {
-    const uint32_t l = pb + uint32_t(w);
-    const uint64_t a = max(claim_off[l], cb), b = min(claim_off[l + 1], ce);
-    if (a >= b) continue;
-    const uint64_t lb = off[l], le = off[l + 1];
-    if (lb == le) continue;
-    const uint32_t lmax = __ldg(col + le - 1);
-    for (uint64_t c = a + lane; c < b; c += 32) {
-      const uint64_t wv = win[c];
-      if (skip_neg && (wv >> 63)) continue;
-      const uint64_t s = wv & kWinBeginMask;
-      const uint32_t len = uint32_t((wv >> kWinLenShift) & kWinLenMask);
-      if (len <= kShort) {
-        sum += len;
-        continue;
-      }
-      // the windows are nearly tight: most end at or below max N+(l) and are
-      // loaded whole (one load decides); otherwise search the exit position
-      if (__ldg(col + s + len - 1) <= lmax) {
-        sum += len;
-        continue;
-      }
-      uint32_t lo = 0, hi = len - 1;  // first position with an id above lmax (the last one is)
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(col + s + mid) <= lmax) lo = mid + 1; else hi = mid;
-      }
-      sum += min(len, G * (lo / G + 1));
+  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < P.ntasks + P.ncta; w += nwarps) {
+    if (w < P.ntasks) {
+      const uint2 tk = P.tasks[P.gtasks - 1 - (P.toff + w * P.tstride)];
+      for (uint32_t r = tk.x; r < tk.y; ++r) sum += executed_of_record(P.recs[r], P.win, P.col, G, P.skip_neg);
+    } else {
+      sum += executed_of_record(P.crecs[P.toff + (w - P.ntasks) * P.tstride], P.win, P.col, G, P.skip_neg);
     }
   }
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-  if (lane == 0 && sum) atomicAdd(acc, sum);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(out, sum);
 }
 
 // Warp path: the span fits the warp bitmap, or a small pivot (warp hash) with
@@ -1435,6 +1436,8 @@ struct AotPlan {
   DBuf<Rec> wrecs, crecs;
   DBuf<uint2> tasks;
   uint64_t nw = 0, nc = 0, G = 0;
+  // probes_executed of the part (toff, tstride) at group size G (k_executed)
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint64_t> executed;
 };
 
 namespace {
@@ -1702,33 +1705,6 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   const uint64_t T =
       std::max<uint64_t>(kTaskMin, work / (interleave ? nparts : 1) / (uint64_t(std::max(warps, 1)) * 64));
   const bool long_lists = ce > cb && wsum / (ce - cb) >= TL_LONG_WINDOW;
-  // probes_executed of the cut's claims under this run's group size (once per cut)
-  uint32_t group = 32u * uint32_t(long_lists ? (mode == AotMode::count ? kUnrollLong : kUnrollLongEmit) : kUnrollShort);
-  const bool need_executed = !TL_EXEC_COUNT && cut[10] != group;
-  // it runs on the handle's side stream, overlapped with the listing kernel
-  // (it is latency-bound; ~15 ms at C4 when alone), and s joins it before
-  // the counters are read back
-  cudaEvent_t exec_done = nullptr;
-  struct ExecEvGuard {
-    cudaEvent_t& e;
-    ~ExecEvGuard() {
-      if (e) cudaEventDestroy(e);
-    }
-  } exec_guard{exec_done};
-  if (need_executed && ccb < cce) {
-    if (!og.aux) TL_CUDA(cudaStreamCreateWithFlags(&og.aux, cudaStreamNonBlocking));
-    cudaEvent_t ready;
-    TL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    TL_CUDA(cudaEventRecord(ready, s));  // acc zeroed, CP / claims ready
-    TL_CUDA(cudaStreamWaitEvent(og.aux, ready, 0));
-    cudaEventDestroy(ready);
-    k_executed<<<grid_for(uint64_t(cpe - cpb) * 32, 256, 148u * 64u), 256, 0, og.aux>>>(
-        claim_off, og.off.p, og.col.p, cwin, cpb, cpe, ccb, cce, group, skip_negative, acc.p + kExec);
-    TL_CUDA(cudaGetLastError());
-    TL_CUDA(cudaEventCreateWithFlags(&exec_done, cudaEventDisableTiming));
-    TL_CUDA(cudaEventRecord(exec_done, og.aux));
-    ++r.launches;
-  }
   mark("task size");
 
   std::shared_ptr<AotPlan> plan;
@@ -1778,6 +1754,34 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   P.tstride = interleave ? nparts : 1;
   P.ntasks = G > P.toff ? (G - P.toff + P.tstride - 1) / P.tstride : 0;
   P.ncta = nc > P.toff ? (nc - P.toff + P.tstride - 1) / P.tstride : 0;
+  // probes_executed of the records this part runs, at this run's group size:
+  // once per plan and part, on the handle's side stream overlapped with the
+  // listing kernel; s joins it before the counters are read back
+  const uint32_t group =
+      32u * uint32_t(long_lists ? (mode == AotMode::count ? kUnrollLong : kUnrollLongEmit) : kUnrollShort);
+  const auto exec_key = std::make_tuple(P.toff, P.tstride, group);
+  auto exec_it = plan->executed.find(exec_key);
+  const bool need_executed = !TL_EXEC_COUNT && exec_it == plan->executed.end();
+  cudaEvent_t exec_done = nullptr;
+  struct ExecEvGuard {
+    cudaEvent_t& e;
+    ~ExecEvGuard() {
+      if (e) cudaEventDestroy(e);
+    }
+  } exec_guard{exec_done};
+  if (need_executed && P.ntasks + P.ncta) {
+    if (!og.aux) TL_CUDA(cudaStreamCreateWithFlags(&og.aux, cudaStreamNonBlocking));
+    cudaEvent_t ready;
+    TL_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(ready, s));  // acc zeroed, the plan built
+    TL_CUDA(cudaStreamWaitEvent(og.aux, ready, 0));
+    cudaEventDestroy(ready);
+    k_executed<<<grid_for((P.ntasks + P.ncta) * 32, 256, 148u * 64u), 256, 0, og.aux>>>(P, group, acc.p + kExec);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaEventCreateWithFlags(&exec_done, cudaEventDisableTiming));
+    TL_CUDA(cudaEventRecord(exec_done, og.aux));
+    ++r.launches;
+  }
   switch (mode) {
     case AotMode::count: r.launches += launch_kernels<AotMode::count>(P, long_lists, s); break;
     case AotMode::hash: r.launches += launch_kernels<AotMode::hash>(P, long_lists, s); break;
@@ -1813,12 +1817,9 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   TL_CUDA(cudaEventElapsedTime(&r.list_ms, ev[1], ev[2]));
   r.positive = h[kPos];
   r.negative = h[kNeg];
-  if (need_executed) {
-    cut[9] = h[kExec];
-    cut[10] = group;
-  }
   // traversal ids loaded (after the rank-window pruning and the early exit)
-  r.executed = TL_EXEC_COUNT ? h[kExec] : cut[9];
+  if (need_executed) exec_it = plan->executed.emplace(exec_key, h[kExec]).first;
+  r.executed = TL_EXEC_COUNT ? h[kExec] : exec_it->second;
   r.windowed = cut[8] - cut[7];
   if (need_logical) {
     cut[5] = h[kLogical];
