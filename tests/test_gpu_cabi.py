@@ -115,10 +115,23 @@ def test_known_answers():
         assert do.cost_model()["aot_cost"] == 0
         st = do.count()
         assert (st["triangles"], st["probes"]) == (0, 0)
-    # empty graph: all zeros (test_engine.cpp:126-133)
+    # empty graph: all zeros (test_engine.cpp:126-133) -- through every entry point
     do = capi.DeviceGraph.from_pairs(np.zeros((0, 2), np.uint32), 0).orient()
     st = do.count()
     assert (st["triangles"], st["probes"], st["table_builds"]) == (0, 0, 0)
+    assert do.hash()["hash_sum"] == 0 and do.list()[1].shape == (0, 3)
+    batches = []
+    assert do.list_batches(batches.append, batch_triples=10)["triangles"] == 0 and batches == []
+    import torch
+    buf = torch.empty(3, dtype=torch.int32, device="cuda")
+    assert do.list_device(buf.data_ptr(), 0)["triangles"] == 0
+    mg = capi.MultiOriented(do, [0])
+    assert mg.count()["triangles"] == 0 and mg.list()[1].shape == (0, 3)
+    mg.close()
+    # a triangle-free graph with edges (a path) streams no batch either
+    n, e = 6, [(i, i + 1) for i in range(5)]
+    do = capi.DeviceGraph.from_pairs(O.as_pairs(e), n).orient()
+    assert do.list_batches(batches.append, batch_triples=1)["triangles"] == 0 and batches == []
 
 
 def test_complete_graphs_closed_form():  # acceptance.cpp:252-268
