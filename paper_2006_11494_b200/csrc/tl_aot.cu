@@ -1152,12 +1152,12 @@ __global__ void k_logical(const uint32_t* cs, const uint64_t* off, uint64_t cb, 
 // window's last id settles most of them.  One warp per warp task (its records)
 // and per CTA record of this part; run once per plan and part, cached.
 __device__ __forceinline__ unsigned long long executed_of_record(const Rec& R, const uint64_t* win,
-                                                                 const uint32_t* col, uint32_t G, uint32_t skip_neg) {
-  const uint32_t lane = threadIdx.x & 31;
+                                                                 const uint32_t* col, uint32_t G, uint32_t skip_neg,
+                                                                 uint32_t t0, uint32_t step) {
   unsigned long long sum = 0;
   if (R.dl == 0) return 0;
   const uint32_t lmax = __ldg(col + R.lb + R.dl - 1);
-  for (uint64_t c = R.cb + lane; c < R.ce; c += 32) {
+  for (uint64_t c = R.cb + t0; c < R.ce; c += step) {
     const uint64_t wv = win[c];
     if (skip_neg && (wv >> 63)) continue;
     const uint64_t s = wv & kWinBeginMask;
@@ -1176,19 +1176,26 @@ __device__ __forceinline__ unsigned long long executed_of_record(const Rec& R, c
   return sum;
 }
 
+// A CTA record (many claims) gets a whole block, a warp task a warp.
 __global__ void k_executed(Params P, uint32_t G, unsigned long long* out) {
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t wpb = blockDim.x >> 5, tblocks = (P.ntasks + wpb - 1) / wpb;
   unsigned long long sum = 0;
-  for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < P.ntasks + P.ncta; w += nwarps) {
-    if (w < P.ntasks) {
-      const uint2 tk = P.tasks[P.gtasks - 1 - (P.toff + w * P.tstride)];
-      for (uint32_t r = tk.x; r < tk.y; ++r) sum += executed_of_record(P.recs[r], P.win, P.col, G, P.skip_neg);
+  for (uint64_t b = blockIdx.x; b < P.ncta + tblocks; b += gridDim.x) {
+    if (b < P.ncta) {
+      sum += executed_of_record(P.crecs[P.toff + b * P.tstride], P.win, P.col, G, P.skip_neg, threadIdx.x,
+                                blockDim.x);
     } else {
-      sum += executed_of_record(P.crecs[P.toff + (w - P.ntasks) * P.tstride], P.win, P.col, G, P.skip_neg);
+      const uint64_t w = (b - P.ncta) * wpb + (threadIdx.x >> 5);
+      if (w < P.ntasks) {
+        const uint2 tk = P.tasks[P.gtasks - 1 - (P.toff + w * P.tstride)];
+        for (uint32_t r = tk.x; r < tk.y; ++r)
+          sum += executed_of_record(P.recs[r], P.win, P.col, G, P.skip_neg, lane, 32);
+      }
     }
   }
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(out, sum);
+  if (lane == 0 && sum) atomicAdd(out, sum);
 }
 
 // Warp path: the span fits the warp bitmap, or a small pivot (warp hash) with
@@ -1776,7 +1783,8 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     TL_CUDA(cudaEventRecord(ready, s));  // acc zeroed, the plan built
     TL_CUDA(cudaStreamWaitEvent(og.aux, ready, 0));
     cudaEventDestroy(ready);
-    k_executed<<<grid_for((P.ntasks + P.ncta) * 32, 256, 148u * 64u), 256, 0, og.aux>>>(P, group, acc.p + kExec);
+    k_executed<<<unsigned(std::min<uint64_t>(P.ncta + (P.ntasks + 7) / 8, 148u * 64u)), 256, 0, og.aux>>>(
+        P, group, acc.p + kExec);
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaEventCreateWithFlags(&exec_done, cudaEventDisableTiming));
     TL_CUDA(cudaEventRecord(exec_done, og.aux));
