@@ -124,6 +124,11 @@ VARIANTS = {
     # the in-kernel count of loaded traversal ids (off in the product build,
     # which computes probes_executed with k_executed): the two must agree
     "exec_count": ["TL_EXEC_COUNT=1"],
+    # the asynchronous staging of long traversal windows (measured slower,
+    # off in the product build): bulk copies through the TMA engine
+    # (cp.async.bulk + mbarrier) and per-thread cp.async -- kept correct
+    "ring_tma": ["TL_RING=1"],
+    "ring_ldgsts": ["TL_RING=2"],
 }
 
 

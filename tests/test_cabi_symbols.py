@@ -77,3 +77,24 @@ def test_python_binding_mirrors_reference_names(built):
     assert issubclass(trilist.ParseFailure, ValueError)
     g = trilist.Graph()
     assert (g.num_vertices, g.num_edges) == (0, 0)
+
+
+def test_async_staging_variants_carry_their_instructions():
+    """SASS of the ring variants (built here, no GPU needed): the TMA ring's
+    count kernel issues bulk copies (UBLKCP) completed on mbarriers
+    (SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK), the cp.async ring LDGSTS with
+    zero fill; the product build has neither in its count kernel."""
+    import subprocess
+
+    from paper_2006_11494_b200 import _build
+
+    def sass(lib):
+        return subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True,
+                              text=True).stdout
+
+    tma = sass(_build.build_variant("ring_tma"))
+    assert "UBLKCP.S.G" in tma and "SYNCS.ARRIVE.TRANS64" in tma and "SYNCS.PHASECHK.TRANS64" in tma
+    ldgsts = sass(_build.build_variant("ring_ldgsts"))
+    assert "LDGSTS.E.BYPASS.128.ZFILL" in ldgsts
+    prod = sass(_build.build_lib())
+    assert "UBLKCP" not in prod and "LDGSTS" not in prod

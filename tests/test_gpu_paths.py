@@ -36,3 +36,19 @@ def test_every_probe_path_matches_oracle(built):
                 for name in PATHS:
                     work[name] += int(re.search(rf"{name} (\d+)", line).group(1))
     assert all(work[k] > 0 for k in PATHS), work
+
+
+@pytest.mark.parametrize("variant", ["ring_tma", "ring_ldgsts"])
+def test_async_staging_variants_match_oracle(built, variant):
+    """The measured-and-rejected staging of long windows through a per-warp
+    shared-memory ring (TL_RING=1 bulk copies via the TMA engine,
+    TL_RING=2 per-thread cp.async) stays parity-green on the same workload."""
+    from paper_2006_11494_b200 import _build
+
+    lib = _build.build_variant(variant)
+    env = dict(os.environ, TL_LIB_PATH=lib)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py"), "--size", "medium"],
+                       env=env, capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, (variant, p.stderr[-3000:])
+    assert "rmat17 ok" in p.stdout and "ingest ok" in p.stdout
+
