@@ -407,6 +407,58 @@ void append_uint(std::string& out, std::uint32_t x) {
   out.append(buf, p);
 }
 
+// Unsorted `list`: the lines are written batch by batch as the device lists
+// them (tl_run_list_batches), so host memory stays bounded whatever the
+// triangle count (the reference builds the whole list first).
+struct ListWriter {
+  FILE* f;
+  std::string buf;
+  static int write(void* self, const std::uint32_t* t, std::uint64_t count) {
+    auto* w = static_cast<ListWriter*>(self);
+    constexpr std::uint64_t kChunk = 1u << 20;  // lines formatted per write
+    for (std::uint64_t b = 0; b < count; b += kChunk) {
+      const std::uint64_t e = std::min(count, b + kChunk);
+      w->buf.clear();
+      for (std::uint64_t k = b; k < e; ++k) {
+        Triangle tr = canonical_triangle(t[3 * k], t[3 * k + 1], t[3 * k + 2]);
+        append_uint(w->buf, tr.a);
+        w->buf += ' ';
+        append_uint(w->buf, tr.b);
+        w->buf += ' ';
+        append_uint(w->buf, tr.c);
+        w->buf += '\n';
+      }
+      if (std::fwrite(w->buf.data(), 1, w->buf.size(), w->f) != w->buf.size()) return 1;
+    }
+    return 0;
+  }
+};
+
+int stream_list(const CommonArgs& c, const OrientedGraph& og, Algorithm algo) {
+  FILE* f = c.out.empty() ? stdout : std::fopen(c.out.c_str(), "wb");
+  if (!f) {
+    std::fprintf(stderr, "error: cannot open '%s' for writing\n", c.out.c_str());
+    return kExitInput;
+  }
+  ListWriter w{f, {}};
+  int rc = TL_OK;
+  if (og.handle() && og.num_edges()) {
+    tl_run_options o{};
+    o.nparts = 1;
+    o.algorithm = detail::algorithm_code(algo);
+    tl_stats s;
+    rc = tl_run_list_batches(og.handle(), &o, 0, 0, &ListWriter::write, &w, &s);
+  }
+  const bool write_failed = rc == TL_ECANCELED || std::fflush(f) != 0;
+  if (f != stdout) std::fclose(f);
+  if (write_failed) {
+    std::fprintf(stderr, "error: cannot write '%s'\n", c.out.empty() ? "<stdout>" : c.out.c_str());
+    return kExitInput;
+  }
+  check(rc, "list");
+  return kExitOk;
+}
+
 // trilist_main.cpp:227-245: canonical triangles, one "a b c" line each;
 // --sorted sorts them lexicographically (on the device here).
 int cmd_list(const Invocation& inv) {
@@ -422,6 +474,7 @@ int cmd_list(const Invocation& inv) {
   PreparedRun p = prepare(loaded.graph, r, algo, load_s);
   detail::validate(ParallelConfig{r.threads, r.chunk});
   detail::assert_layout(algo, p.oriented);
+  if (!inv.list_sorted) return stream_list(c, p.oriented, algo);
   std::vector<std::uint32_t> tri;
   if (p.oriented.handle() && p.oriented.num_edges()) {
     tl_run_options o{};
