@@ -1638,17 +1638,16 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   const bool interleave = !whole && !spec.range && !(split_mode && std::string(split_mode) == "range") &&
                           spec.algo != Algo::cf_merge;
   const bool cache = !spec.range;  // batched listing walks thousands of ranges once each
-  // ---- the part's cost cut: {cb, ce, pb, pe, table_builds, logical, has_logical, CP[cb], CP[ce],
-  //      executed, group size the executed count was made for (0: none)}
-  std::array<uint64_t, 11> cut_local{};
-  std::array<uint64_t, 11>* cutp = nullptr;
+  // ---- the part's cost cut: {cb, ce, pb, pe, table_builds, logical, has_logical, CP[cb], CP[ce]}
+  std::array<uint64_t, 9> cut_local{};
+  std::array<uint64_t, 9>* cutp = nullptr;
   const auto cut_key = std::make_tuple(cp_key, whole ? 0u : part, whole ? 1u : nparts);
   if (cache) {
     auto it = og.cuts.find(cut_key);
     if (it != og.cuts.end()) cutp = &it->second;
   }
   if (!cutp) {
-    std::array<uint64_t, 11> c{};
+    std::array<uint64_t, 9> c{};
     uint64_t hs[8] = {0, m, 0, og.n, 0, 0, m, 0};
     DBuf<uint64_t> split;
     split.alloc(8, s);
@@ -1678,7 +1677,7 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
       cutp = &cut_local;
     }
   }
-  std::array<uint64_t, 11>& cut = *cutp;
+  std::array<uint64_t, 9>& cut = *cutp;
   const uint64_t ccb = cut[0], cce = cut[1];
   const uint32_t cpb = uint32_t(cut[2]), cpe = uint32_t(cut[3]);
   r.table_builds = cut[4];

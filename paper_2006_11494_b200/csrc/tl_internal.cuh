@@ -69,7 +69,7 @@ struct tl_oriented {
   // ve, table_builds, logical, has_logical} -- and the work records + tasks per
   // (claim set, claim range, task size).  A step of a partitioned run then
   // rebuilds nothing.
-  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::array<uint64_t, 11>> cuts;
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::array<uint64_t, 9>> cuts;
   std::map<std::tuple<uint32_t, uint64_t, uint64_t, uint64_t>, std::shared_ptr<tlb::AotPlan>> plans;
   ~tl_oriented();
 };
