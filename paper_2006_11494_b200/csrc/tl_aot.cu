@@ -52,13 +52,13 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #define TL_UNROLL 4
 #endif
 #ifndef TL_UNROLL_LONG
-#define TL_UNROLL_LONG 6
+#define TL_UNROLL_LONG 8
 #endif
 #ifndef TL_LONG_WINDOW
 #define TL_LONG_WINDOW 160
 #endif
 #ifndef TL_WARP_WORDS
-#define TL_WARP_WORDS 1280  // per-warp probe region in 32-bit words (5 KB: a 40,960-bit span)
+#define TL_WARP_WORDS 1184  // per-warp probe region in 32-bit words (a 37,888-bit span): 5 CTAs then fit the 196 KB carve-out
 #endif
 #ifndef TL_CTAS_PER_SM
 #define TL_CTAS_PER_SM 5
@@ -67,7 +67,7 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 #define TL_CTA_MIN_WORK 65536
 #endif
 #ifndef TL_EMIT_UNROLL_LONG
-#define TL_EMIT_UNROLL_LONG TL_UNROLL_LONG
+#define TL_EMIT_UNROLL_LONG 6
 #endif
 constexpr int kUnrollShort = TL_UNROLL;
 constexpr int kUnrollLong = TL_UNROLL_LONG;
@@ -148,6 +148,9 @@ constexpr bool kRingAsync = TL_RING == 2;  // 2: per-thread cp.async (LDGSTS); 1
 static_assert(!kRingAsync || kRingWords % 128 == 0, "LDGSTS chunks are 128-word multiples");
 static_assert((kRingWords & (kRingWords - 1)) == 0 && kRingWords >= 32 && kRingWords <= 256, "ring chunk size");
 
+#ifndef TL_REDUX_FOLD
+#define TL_REDUX_FOLD 1
+#endif
 #ifndef TL_FLUSH_UNROLL
 #define TL_FLUSH_UNROLL 4
 #endif
@@ -264,6 +267,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(__cvta_generic_to_global(p)));
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -291,16 +297,56 @@ __device__ __forceinline__ uint32_t cas_sm(uint32_t a, uint32_t cmp, uint32_t v)
 }
 
 // ------------------------------------------------------------ probe sides
+// The C4 count kernel kept the ALU pipe (LOP3 / SHF / IADD3 / ISETP /
+// VIADDMNMX) 64% busy under ncu (profiles/r2_ncu_summary_c4.md) while the FMA
+// pipe idled; both issue one warp instruction per 2 cycles per SM
+// sub-partition and run side by side (tools/pipe_bench.cu, profiles/
+// r2_pipe_bench.txt).  TL_FMA_PROBE=1 builds the bitmap probe with fewer ALU
+// instructions: the word's byte address is one multiply-add of d >> 5 (IMAD,
+// the multiplier read from the constant bank so ptxas keeps it on the FMA
+// pipe), the bitmap stores id d at bit 31 - (d & 31) so one rotate (SHF.L.W)
+// brings it to bit 31, and the count adds t >> 31 (one LEA.HI): 4 ALU + 1 FMA
+// instructions per id instead of 5.5 + 1.  IMAD.HI / mad.hi forms of the
+// shift and of the accumulation were also built and are slower: IMAD.HI
+// issues at a quarter rate.
+#ifndef TL_FMA_PROBE
+#define TL_FMA_PROBE 1
+#endif
+#ifndef TL_OPAQUE_BASE
+#define TL_OPAQUE_BASE 1
+#endif
+__constant__ uint32_t c_mul4 = 4u;
+__device__ __forceinline__ uint32_t mad_lo_c4(uint32_t a, uint32_t c) {  // 4 * a + c on the FMA pipe
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(c_mul4), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t rotl_wrap(uint32_t a, uint32_t s) {  // bit 31 - (s & 31) lands in bit 31
+  uint32_t r;
+  asm("shf.l.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(a), "r"(s));
+  return r;
+}
+
 struct BitmapProbe {  // bit (x - lmin) of the words at byte address `base`
   static constexpr bool kRangeChecked = true;  // bit() itself rejects x outside [lmin, lmax]
   uint32_t base, lmin, span;
   // Branch-free membership as 0/1 with one LDS.  Ids outside [lmin, lmax]
   // clamp to bit `span`, which is never set (the region keeps a zero word past
   // the largest span).
+#if TL_FMA_PROBE
+  static constexpr uint32_t mask(uint32_t d) { return 0x80000000u >> (d & 31); }
+  __device__ __forceinline__ uint32_t bit(uint32_t x) const {
+    const uint32_t d = min(x - lmin, span);
+    return rotl_wrap(ld_sm(mad_lo_c4(d >> 5, base)), d) >> 31;
+  }
+#else
+  static constexpr uint32_t mask(uint32_t d) { return 1u << (d & 31); }
   __device__ __forceinline__ uint32_t bit(uint32_t x) const {
     const uint32_t d = min(x - lmin, span);
     return (ld_sm(base + ((d >> 5) << 2)) >> (d & 31)) & 1u;
   }
+#endif
+  __device__ __forceinline__ uint32_t add(uint32_t x, uint32_t hits) const { return hits + bit(x); }
   __device__ __forceinline__ bool test(uint32_t x) const { return bit(x) != 0; }
 };
 
@@ -342,6 +388,7 @@ struct RankProbe {
     }
     return hit;
   }
+  __device__ __forceinline__ uint32_t add(uint32_t x, uint32_t hits) const { return hits + bit(x); }
   __device__ __forceinline__ bool test(uint32_t x) const { return bit(x) != 0; }
 };
 
@@ -473,7 +520,7 @@ struct GlobalProbe {  // pivots beyond every shared-memory layout
 
 __device__ __forceinline__ void bitmap_set(uint32_t base, uint32_t lmin, uint32_t x) {
   const uint32_t d = x - lmin;
-  red_or_sm(base + ((d >> 5) << 2), 1u << (d & 31));
+  red_or_sm(base + ((d >> 5) << 2), BitmapProbe::mask(d));
 }
 __device__ __forceinline__ void bitmap_clear(uint32_t base, uint32_t lmin, uint32_t x) {
   st_sm(base + (((x - lmin) >> 5) << 2), 0u);
@@ -501,9 +548,20 @@ struct Lane {
   uint32_t ring = 0;    // ring modes: byte address of the warp's chunk ring
   uint32_t bars = 0;    //             and of its per-stage mbarriers
   uint32_t phases = 0;  //             bit s = parity of stage s's next completion
+  // Per record: the lanes' 32-bit counts go to 64-bit totals.  TL_REDUX_FOLD=1
+  // sums them across the warp first (REDUX.SUM), so the totals are
+  // warp-uniform and live in uniform registers instead of four registers per
+  // lane (the 48-register count kernel then keeps all U loads of a group in
+  // flight).  A record's hits fit 32 bits: its weight is bounded by the task
+  // size plus one claim window (< 2^23 ids), and tasks are sized far below 2^31.
   __device__ __forceinline__ void fold() {
+#if TL_REDUX_FOLD
+    pos64 += __reduce_add_sync(kFull, pos);
+    neg64 += __reduce_add_sync(kFull, neg);
+#else
     pos64 += pos;
     neg64 += neg;
+#endif
     pos = neg = 0;
   }
 };
@@ -609,6 +667,18 @@ __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint
 }
 
 // ------------------------------------------------------------ claim batch
+// TL_PREFETCH: L2 prefetches of the traversal windows a claim batch is about
+// to read -- 1: the next long list while the current one is swept; 2: also
+// the batch's first long list, under the packed rounds; 3: also the first and
+// last line of every packed (short) claim.  0 = off.
+#ifndef TL_PREFETCH
+#define TL_PREFETCH 3
+#endif
+// TL_PIPE=1: count mode sweeps a batch's long lists as one software-pipelined
+// stream of groups (claim_batch); 0: one list at a time, load then probe.
+#ifndef TL_PIPE
+#define TL_PIPE 1
+#endif
 template <AotMode MODE, int U>
 constexpr bool kOverLast() {
   return !(MODE == AotMode::count && U == kUnrollLong);
@@ -747,6 +817,25 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit)) | (MODE == AotMode::list && P.swap_neg && neg ? kSwapBit : 0u);
   }
 
+#if TL_PREFETCH
+  // The next long list's lines are requested into L2 while the current one is
+  // swept (lane i asks for the line of its i-th round: up to 1024 ids), so its
+  // demand loads find them there or on their way: more bytes in flight per
+  // warp without holding registers.
+  auto prefetch_list = [&](unsigned m) {
+    if (m) {
+      const int jn = __ffs(m) - 1;
+      const uint64_t bn = __shfl_sync(kFull, b, jn);
+      const uint32_t ln = __shfl_sync(kFull, len, jn);
+      if (32 * lane < ln + 31) prefetch_l2(P.col + bn + 32 * lane);
+    }
+  };
+  if (TL_PREFETCH >= 2) prefetch_list(__ballot_sync(kFull, len > kShort));  // the first long list, under the packed rounds
+  if (TL_PREFETCH >= 3 && len && len <= kShort) {  // the packed claims' lines (rounds after the first find them in L2)
+    prefetch_l2(P.col + b);
+    prefetch_l2(P.col + b + len - 1);
+  }
+#endif
   // ---- short claims: 32 probes per round, load-balanced over the lanes
   const uint32_t slen = len > kShort ? 0 : len;
   uint32_t incl = slen;
@@ -799,9 +888,71 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   // ---- long claims: the whole warp sweeps one list, U rounds of 32
   // loads in flight; lists are rank-ascending, so a list is abandoned once a
   // group reaches past max N+(l)
+  if constexpr (TL_PIPE && MODE == AotMode::count) {
+    // Software-pipelined over the batch's long lists as one stream of groups:
+    // a group's registers are reloaded with the next group -- of the same
+    // list, or the first group of the next list once this one ends -- while
+    // the group is probed, so the next loads fly under this group's probes
+    // and a list's first round trip overlaps the previous list's last group.
+    // The group's last round decides the early exit first (ids ascend across
+    // rounds and lanes; kEmpty past the window's end also ends the list),
+    // which also orders all U loads of a group before their first use.
+    // (Emission modes keep the probed ids for the staged hits; a second
+    // register set for the next group measured +2% at C4 hash, -2% at C3.)
+    if (!longm) return;
+    int j = __ffs(longm) - 1;
+    longm &= longm - 1;
+    const uint32_t* p = P.col + __shfl_sync(kFull, b, j) + lane;
+    uint32_t lcur = __shfl_sync(kFull, len, j);
+    int rem = int(lcur) - int(lane);  // this lane reads p[32k] while 32k < rem
+    bool nj = __shfl_sync(kFull, neg, j);
+    uint32_t x[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+    uint32_t hits = 0, groups = 0;
+    while (true) {
+      const bool stop = __any_sync(kFull, x[U - 1] > lmax);  // the current list's last group
+      const bool cneg = nj;
+      const uint32_t lprev = lcur;
+      bool more = true;
+      if (stop) {
+        more = longm != 0;
+        if (more) {
+          j = __ffs(longm) - 1;
+          longm &= longm - 1;
+          p = P.col + __shfl_sync(kFull, b, j) + lane - 32 * U;
+          lcur = __shfl_sync(kFull, len, j);
+          rem = int(lcur) - int(lane) + 32 * U;
+          nj = __shfl_sync(kFull, neg, j);
+        } else {
+          rem = 0;  // nothing left to load
+        }
+      }
+      p += 32 * U;
+      rem -= 32 * U;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
+        else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
+        x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+      }
+      ++groups;
+      if (stop) {
+        if (cneg) st.neg += hits; else st.pos += hits;
+        if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), min(lprev, 32 * U * groups));  // ids loaded
+        hits = 0;
+        groups = 0;
+        if (!more) break;
+      }
+    }
+    return;
+  }
   while (longm) {
     const int j = __ffs(longm) - 1;
     longm &= longm - 1;
+#if TL_PREFETCH
+    prefetch_list(longm);
+#endif
     const uint64_t bj = __shfl_sync(kFull, b, j);
     const uint32_t lj = __shfl_sync(kFull, len, j);
     const bool nj = __shfl_sync(kFull, neg, j);
@@ -828,9 +979,13 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
         } else {
           over |= x[k] > lmax;
         }
-        const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
-        hits += hit;
-        if constexpr (MODE != AotMode::count) hm |= hit << k;
+        if constexpr (MODE == AotMode::count && Probe::kRangeChecked) {
+          hits = probe.add(x[k], hits);
+        } else {
+          const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
+          hits += hit;
+          if constexpr (MODE != AotMode::count) hm |= hit << k;
+        }
       }
       if constexpr (MODE != AotMode::count) emit_group<MODE, U>(st, P, hm, x, SameWord<U>{oj});
       p += 32 * U;
@@ -850,7 +1005,7 @@ __device__ __forceinline__ void reduce_and_flush(Lane<MODE>& st, const Params& P
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[k] += __shfl_xor_sync(kFull, v[k], o);
+    for (int k = TL_REDUX_FOLD ? 2 : 0; k < 3; ++k) v[k] += __shfl_xor_sync(kFull, v[k], o);  // folded totals are already the warp's
     v[3] ^= __shfl_xor_sync(kFull, v[3], o);
   }
   if (lane_id() == 0) {
@@ -1018,7 +1173,10 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_
                                                                                   : TL_LIST_CTAS) k_aot(Params P) {
   __shared__ unsigned long long s_task;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t wbase = sm_addr(warp * kWarpStride);
+  uint32_t wbase = sm_addr(warp * kWarpStride);
+#if TL_OPAQUE_BASE
+  asm volatile("mov.u32 %0, %0;" : "+r"(wbase));  // held in a register, not rebuilt from SR_CgaCtaId in the hot loop
+#endif
   for (uint32_t i = lane; i < kWarpStride; i += 32) st_sm(wbase + 4 * i, 0u);
   if constexpr (TL_EXEC_COUNT)
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(__cvta_shared_to_generic(exec_addr())) = 0ull;
@@ -1037,7 +1195,10 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_
   __syncthreads();
   // ---- phase 1: CTA records
   if (P.ncta) {
-    const uint32_t cbase = sm_addr(0);
+    uint32_t cbase = sm_addr(0);
+#if TL_OPAQUE_BASE
+    asm volatile("mov.u32 %0, %0;" : "+r"(cbase));
+#endif
     while (true) {
       if (threadIdx.x == 0) s_task = atomicAdd(P.acc + kCtaCounter, 1ull);
       __syncthreads();  // also orders the previous record's clear before the next build
