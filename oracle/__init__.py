@@ -59,6 +59,10 @@ def olib() -> C.CDLL:
     L.or_draw.argtypes = [C.c_uint64, C.c_uint64]
     L.or_triangle_hash.restype = C.c_uint64
     L.or_triangle_hash.argtypes = [C.c_uint32] * 3
+    L.or_triangle_hash_xor.restype = C.c_uint64
+    L.or_triangle_hash_xor.argtypes = [C.c_uint32] * 3
+    L.or_vertex_word.restype = C.c_uint64
+    L.or_vertex_word.argtypes = [C.c_uint32]
     L.or_permute_id.restype = C.c_uint32
     L.or_permute_id.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32]
     L.or_gen_er.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, u32p]
@@ -107,7 +111,17 @@ def fmix64(z: int) -> int:
 
 
 def triangle_hash(a: int, b: int, c: int) -> int:
+    """The triangle's hash_sum term Z(a) Z(b) Z(c) mod 2^64."""
     return olib().or_triangle_hash(a, b, c)
+
+
+def triangle_hash_xor(a: int, b: int, c: int) -> int:
+    """The triangle's hash_xor term Z(a) & Z(b) & Z(c)."""
+    return olib().or_triangle_hash_xor(a, b, c)
+
+
+def vertex_word(v: int) -> int:
+    return olib().or_vertex_word(v)
 
 
 def gen_er(seed: int, n: int, npairs: int) -> np.ndarray:
@@ -374,10 +388,13 @@ def hash_of_triples(canon: np.ndarray):
             z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
             return z ^ (z >> np.uint64(31))
 
-    h = mix(mix((a << np.uint64(32)) | b) ^ c)
+    # Z(v) = fmix64(v + golden); sum of Z(a) Z(b) Z(c) mod 2^64, xor of Z(a) & Z(b) & Z(c)
     with np.errstate(over="ignore"):
+        za, zb, zc = (mix(v + np.uint64(0x9E3779B97F4A7C15)) for v in (a, b, c))
+        h = za * zb * zc
         s = int(np.sum(h, dtype=np.uint64)) if h.size else 0
-    x = int(np.bitwise_xor.reduce(h)) if h.size else 0
+    hx = za & zb & zc
+    x = int(np.bitwise_xor.reduce(hx)) if hx.size else 0
     return len(h), s, x
 
 

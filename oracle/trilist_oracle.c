@@ -34,10 +34,17 @@ OR_API uint64_t or_fmix64(uint64_t z) {
 /* k-th output (0-based) of the sequential splitmix64 seeded with `seed`. */
 OR_API uint64_t or_draw(uint64_t seed, uint64_t k) { return or_fmix64(seed + (k + 1) * kGolden); }
 
-/* Order-independent triangle hash over a canonical
- * (a<b<c) original-id triple. */
-OR_API uint64_t or_triangle_hash(uint32_t a, uint32_t b, uint32_t c) {
-  return or_fmix64(or_fmix64(((uint64_t)a << 32) | b) ^ (uint64_t)c);
+/* Order-independent triangle hash (round-2 definition,
+ * the one oracle/ref_shim.cpp's HashSink applies to the reference's own
+ * emissions): every vertex has the word Z(v) = fmix64(v + golden) of its
+ * original id; a triangle adds Z(a) Z(b) Z(c) mod 2^64 to hash_sum and xors
+ * Z(a) & Z(b) & Z(c) into hash_xor.  Both are symmetric in the three ids. */
+OR_API uint64_t or_vertex_word(uint32_t v) { return or_fmix64((uint64_t)v + kGolden); }
+OR_API uint64_t or_triangle_hash_xor(uint32_t a, uint32_t b, uint32_t c) {
+  return or_vertex_word(a) & or_vertex_word(b) & or_vertex_word(c);
+}
+OR_API uint64_t or_triangle_hash(uint32_t a, uint32_t b, uint32_t c) {  /* the hash_sum term */
+  return or_vertex_word(a) * or_vertex_word(b) * or_vertex_word(c);
 }
 
 static void canon3(uint32_t* x, uint32_t* y, uint32_t* z) { /* graph.cpp:148-153 */
@@ -395,8 +402,8 @@ OR_API uint64_t or_aot(const or_oriented* g, int skip_negative, uint64_t* stats,
     }                                                                       \
     emitted++;                                                              \
     canon3(&e0_, &e1_, &e2_);                                               \
-    uint64_t h = or_triangle_hash(e0_, e1_, e2_);                           \
-    s[6] += h; s[7] ^= h;                                                   \
+    s[6] += or_triangle_hash(e0_, e1_, e2_);                                \
+    s[7] ^= or_triangle_hash_xor(e0_, e1_, e2_);                            \
   } while (0)
   for (uint32_t u = 0; u < g->n; ++u) {
     uint64_t ub = g->out_off[u], ue = g->out_off[u + 1];
@@ -454,8 +461,8 @@ OR_API uint64_t or_kernel(const or_oriented* g, int algo, int reuse, uint64_t* s
     }                                                                       \
     emitted++;                                                              \
     canon3(&e0_, &e1_, &e2_);                                               \
-    uint64_t h = or_triangle_hash(e0_, e1_, e2_);                           \
-    s[6] += h; s[7] ^= h;                                                   \
+    s[6] += or_triangle_hash(e0_, e1_, e2_);                                \
+    s[7] ^= or_triangle_hash_xor(e0_, e1_, e2_);                            \
   } while (0)
 #define OR_SET(list_b, list_e, on)                                          \
   for (uint64_t q_ = (list_b); q_ < (list_e); ++q_) {                       \

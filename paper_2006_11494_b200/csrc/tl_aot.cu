@@ -194,6 +194,7 @@ struct Params {
   const uint64_t* win;     // claim windows {begin:40 | len:23 | neg:1}
   const uint32_t* cs;      // traversed vertex per claim (hash/list modes)
   const uint32_t* orig;
+  const uint64_t* vword;  // hash mode: rank -> vertex_word(original id)
   const Rec* recs;      // phase 2 (warp) records
   const uint2* tasks;   // phase 2: [rb, re) record ranges
   uint64_t ntasks;       // this part's warp tasks: global index gtasks - 1 - (toff + t * tstride)
@@ -545,6 +546,7 @@ struct Lane {
   uint32_t ebase = 0;   // hash/list: byte address of the per-warp staging buffer
   uint32_t ecount = 0;  // warp-uniform
   uint32_t a_orig = 0;  // the current record's pivot (original id)
+  unsigned long long zl = 0;  // hash mode: the pivot's vertex word
   uint32_t ring = 0;    // ring modes: byte address of the warp's chunk ring
   uint32_t bars = 0;    //             and of its per-stage mbarriers
   uint32_t phases = 0;  //             bit s = parity of stage s's next completion
@@ -575,38 +577,29 @@ __device__ __forceinline__ uint2 ld_sm2(uint32_t a) {
   return v;
 }
 
-// A flush maps the witnesses to original ids with independent gathers (all
-// in flight at once) and then hashes or writes the whole batch.
+// List mode: a flush maps the witnesses to original ids with independent
+// gathers (all in flight at once) and writes the whole batch.  (Hash mode
+// stages nothing: tl_common.cuh's hash distributes over a claim's hits.)
 template <AotMode MODE>
 __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
-  if constexpr (MODE != AotMode::count) {
+  if constexpr (MODE == AotMode::list) {
     __syncwarp();
     const uint32_t cnt = st.ecount;
     if (cnt) {
       unsigned long long base = 0;
-      if constexpr (MODE == AotMode::list) {
-        if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
-        base = __shfl_sync(kFull, base, 0);
-      }
+      if (lane_id() == 0) base = atomicAdd(P.acc + kEmitted, (unsigned long long)cnt);
+      base = __shfl_sync(kFull, base, 0);
 #pragma unroll kFlushUnroll
       for (uint32_t i = lane_id(); i < cnt; i += 32) {
         const uint2 e = ld_sm2(st.ebase + 8 * i);
-        uint32_t c = __ldg(P.orig + e.y);
-        if constexpr (MODE == AotMode::list) {
-          const uint32_t b = e.x & ~kSwapBit;
-          const bool sw = e.x & kSwapBit;
-          if (base + i < P.out_cap) {
-            uint32_t* o = P.out + 3 * (base + i);
-            o[0] = sw ? b : st.a_orig;
-            o[1] = sw ? st.a_orig : b;
-            o[2] = c;
-          }
-        } else {
-          uint32_t a = st.a_orig, b = e.x;
-          canon3(a, b, c);
-          const uint64_t h = tri_hash(a, b, c);
-          st.hsum += h;
-          st.hxor ^= h;
+        const uint32_t c = __ldg(P.orig + e.y);
+        const uint32_t b = e.x & ~kSwapBit;
+        const bool sw = e.x & kSwapBit;
+        if (base + i < P.out_cap) {
+          uint32_t* o = P.out + 3 * (base + i);
+          o[0] = sw ? b : st.a_orig;
+          o[1] = sw ? st.a_orig : b;
+          o[2] = c;
         }
       }
     }
@@ -618,11 +611,12 @@ __device__ __forceinline__ void flush_emits(Lane<MODE>& st, const Params& P) {
 // Starts a record: the previous record's hits go out with its pivot.
 template <AotMode MODE>
 __device__ __forceinline__ void begin_record(Lane<MODE>& st, const Params& P, uint32_t l) {
-  if constexpr (MODE != AotMode::count) {
+  if constexpr (MODE == AotMode::list) {
     const uint32_t a = __ldg(P.orig + l);
     if (a != st.a_orig && st.ecount) flush_emits(st, P);
     st.a_orig = a;
   }
+  if constexpr (MODE == AotMode::hash) st.zl = __ldg(P.vword + l);
 }
 
 // Warp-collective: the hits of one group of U sweep rounds of one list (bit
@@ -678,6 +672,9 @@ __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint
 // stream of groups (claim_batch); 0: one list at a time, load then probe.
 #ifndef TL_PIPE
 #define TL_PIPE 1
+#endif
+#ifndef TL_PIPE_HASH
+#define TL_PIPE_HASH 0
 #endif
 template <AotMode MODE, int U>
 constexpr bool kOverLast() {
@@ -812,9 +809,19 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     len = (P.skip_neg && neg) ? 0u : uint32_t((w >> kWinLenShift) & kWinLenMask);
   }
   const uint32_t sflag = neg ? kNegBit : 0u;
-  uint32_t b_orig = 0;  // neighbour word: original id | swap (list-mode cf-hash negative claim)
-  if constexpr (MODE != AotMode::count) {
-    if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit)) | (MODE == AotMode::list && P.swap_neg && neg ? kSwapBit : 0u);
+  uint32_t b_orig = 0;  // list mode's neighbour word: original id | swap (cf-hash negative claim)
+  if constexpr (MODE == AotMode::list) {
+    if (len) b_orig = __ldg(P.orig + (P.cs[c] & ~kNegBit)) | (P.swap_neg && neg ? kSwapBit : 0u);
+  }
+  // hash mode: the claim's factors Z(l) Z(s) and Z(l) & Z(s); its hits w add
+  // Z(w) times the first to hash_sum and Z(w) & the second to hash_xor
+  unsigned long long fmul = 0, fand = 0;
+  if constexpr (MODE == AotMode::hash) {
+    if (len) {
+      const unsigned long long zs = __ldg(P.vword + (P.cs[c] & ~kNegBit));
+      fmul = st.zl * zs;
+      fand = st.zl & zs;
+    }
   }
 
 #if TL_PREFETCH
@@ -853,7 +860,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
 #endif
   constexpr int kSU = TL_SHORT_UNROLL;  // packed rounds in flight
   for (uint32_t r0 = 0; r0 < total; r0 += 32 * kSU) {
-    uint32_t x[kSU], of[kSU], oo[kSU];
+    uint32_t x[kSU], of[kSU], oo[kSU];  // oo: list mode the owner's neighbour word, hash mode the owner lane
 #pragma unroll
     for (int k = 0; k < kSU; ++k) {
       const uint32_t q = r0 + 32 * k + lane;
@@ -866,7 +873,8 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       const uint64_t obm = __shfl_sync(kFull, bm, i);
       of[k] = __shfl_sync(kFull, sflag, i);
       oo[k] = 0;
-      if constexpr (MODE != AotMode::count) oo[k] = __shfl_sync(kFull, b_orig, i);
+      if constexpr (MODE == AotMode::list) oo[k] = __shfl_sync(kFull, b_orig, i);
+      if constexpr (MODE == AotMode::hash) oo[k] = i;
       x[k] = q < total ? __ldg(P.col + obm + q) : kEmpty;
     }
     uint32_t hm = 0;
@@ -876,7 +884,17 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       if (of[k] & kNegBit) st.neg += hit; else st.pos += hit;
       if constexpr (MODE != AotMode::count) hm |= hit << k;
     }
-    if constexpr (MODE != AotMode::count) emit_group<MODE, kSU>(st, P, hm, x, RoundWords<kSU>{oo});
+    if constexpr (MODE == AotMode::list) emit_group<MODE, kSU>(st, P, hm, x, RoundWords<kSU>{oo});
+    if constexpr (MODE == AotMode::hash) {
+      unsigned long long z[kSU];
+#pragma unroll
+      for (int k = 0; k < kSU; ++k) z[k] = (hm >> k) & 1u ? __ldg(P.vword + x[k]) : 0ull;
+#pragma unroll
+      for (int k = 0; k < kSU; ++k) {
+        st.hsum += z[k] * __shfl_sync(kFull, fmul, oo[k]);
+        st.hxor ^= z[k] & __shfl_sync(kFull, fand, oo[k]);
+      }
+    }
     (void)hm;
   }
 
@@ -888,7 +906,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   // ---- long claims: the whole warp sweeps one list, U rounds of 32
   // loads in flight; lists are rank-ascending, so a list is abandoned once a
   // group reaches past max N+(l)
-  if constexpr (TL_PIPE && MODE == AotMode::count) {
+  if constexpr (TL_PIPE && (MODE == AotMode::count || (TL_PIPE_HASH && MODE == AotMode::hash))) {
     // Software-pipelined over the batch's long lists as one stream of groups:
     // a group's registers are reloaded with the next group -- of the same
     // list, or the first group of the next list once this one ends -- while
@@ -897,8 +915,9 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     // The group's last round decides the early exit first (ids ascend across
     // rounds and lanes; kEmpty past the window's end also ends the list),
     // which also orders all U loads of a group before their first use.
-    // (Emission modes keep the probed ids for the staged hits; a second
-    // register set for the next group measured +2% at C4 hash, -2% at C3.)
+    // Hash mode gathers a hit's vertex word before its id's register is
+    // reloaded and adds the group's words after the reloads are issued.  (List
+    // mode keeps the probed ids for the staged hits.)
     if (!longm) return;
     int j = __ffs(longm) - 1;
     longm &= longm - 1;
@@ -910,10 +929,12 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
 #pragma unroll
     for (int k = 0; k < U; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
     uint32_t hits = 0, groups = 0;
+    unsigned long long zsum = 0, zxor = 0;  // hash mode: this lane's witnesses' words of the current list
     while (true) {
       const bool stop = __any_sync(kFull, x[U - 1] > lmax);  // the current list's last group
       const bool cneg = nj;
       const uint32_t lprev = lcur;
+      const int jprev = j;
       bool more = true;
       if (stop) {
         more = longm != 0;
@@ -930,15 +951,36 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       }
       p += 32 * U;
       rem -= 32 * U;
+      if constexpr (MODE == AotMode::hash) {
+        unsigned long long z[U];
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
-        else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
-        x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+        for (int k = 0; k < U; ++k) {
+          const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
+          hits += hit;
+          z[k] = hit ? __ldg(P.vword + x[k]) : 0ull;
+          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          zsum += z[k];
+          zxor ^= z[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
+          else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
+          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+        }
       }
       ++groups;
       if (stop) {
         if (cneg) st.neg += hits; else st.pos += hits;
+        if constexpr (MODE == AotMode::hash) {
+          st.hsum += zsum * __shfl_sync(kFull, fmul, jprev);
+          st.hxor ^= zxor & __shfl_sync(kFull, fand, jprev);
+          zsum = zxor = 0;
+        }
         if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), min(lprev, 32 * U * groups));  // ids loaded
         hits = 0;
         groups = 0;
@@ -957,7 +999,8 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     const uint32_t lj = __shfl_sync(kFull, len, j);
     const bool nj = __shfl_sync(kFull, neg, j);
     uint32_t oj = 0;
-    if constexpr (MODE != AotMode::count) oj = __shfl_sync(kFull, b_orig, j);
+    if constexpr (MODE == AotMode::list) oj = __shfl_sync(kFull, b_orig, j);
+    unsigned long long zsum = 0, zxor = 0;  // hash mode: this lane's witnesses' words of list j
     const uint32_t* p = P.col + bj + lane;
     int rem = int(lj) - int(lane);  // this lane reads p[32k] while 32k < rem
     uint32_t hits = 0;
@@ -987,12 +1030,26 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
           if constexpr (MODE != AotMode::count) hm |= hit << k;
         }
       }
-      if constexpr (MODE != AotMode::count) emit_group<MODE, U>(st, P, hm, x, SameWord<U>{oj});
+      if constexpr (MODE == AotMode::list) emit_group<MODE, U>(st, P, hm, x, SameWord<U>{oj});
+      if constexpr (MODE == AotMode::hash) {
+        unsigned long long z[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) z[k] = (hm >> k) & 1u ? __ldg(P.vword + x[k]) : 0ull;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          zsum += z[k];
+          zxor ^= z[k];
+        }
+      }
       p += 32 * U;
       rem -= 32 * U;
       if (__any_sync(kFull, over)) break;
     }
     if (nj) st.neg += hits; else st.pos += hits;
+    if constexpr (MODE == AotMode::hash) {
+      st.hsum += zsum * __shfl_sync(kFull, fmul, j);
+      st.hxor ^= zxor & __shfl_sync(kFull, fand, j);
+    }
     if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), min(lj, uint32_t(int(lj) - rem)));  // ids loaded
   }
 }
@@ -1184,7 +1241,7 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_
   st.ebase = sm_addr(kWarpsPerCta * kWarpStride + warp * (2 * emit_cap<MODE>()));
   if constexpr (ring_mode<MODE>()) {
     constexpr uint32_t off =
-        (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
+        (kWarpsPerCta * kWarpStride + (MODE == AotMode::list ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
     st.bars = sm_addr(off + warp * 2 * kRingStages);
     st.ring = sm_addr(off + ((kWarpsPerCta * 2 * kRingStages + 31) & ~31u) + warp * kRingStages * kRingWords);
     if (lane == 0) {
@@ -1223,6 +1280,11 @@ __global__ void __launch_bounds__(kWarpThreads, MODE == AotMode::count  ? (ring_
 // ------------------------------------------------------------ work building
 #define TL_GRID_STRIDE(i, count) \
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (count); i += uint64_t(gridDim.x) * blockDim.x)
+
+// rank -> vertex_word(original id) (tl_common.cuh): the hash sink gathers one per triangle
+__global__ void k_vertex_words(const uint32_t* orig, uint32_t n, uint64_t* vword) {
+  TL_GRID_STRIDE(i, uint64_t(n)) vword[i] = vertex_word(orig[i]);
+}
 
 // Claim cost (the window's length, an upper bound of its probes; 0 for a
 // skipped negative claim), for claim i < m; 0 at i = m so an exclusive scan of
@@ -1549,11 +1611,11 @@ int sm_count() {
 // warps' hit staging, then (ring modes) the stage mbarriers and the rings.
 template <AotMode MODE>
 __host__ __device__ constexpr uint32_t ring_words_offset() {  // 32-word (128 B) aligned
-  return (kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
+  return (kWarpsPerCta * kWarpStride + (MODE == AotMode::list ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0) + 31) & ~31u;
 }
 template <AotMode MODE>
 size_t kernel_smem() {
-  uint32_t words = kWarpsPerCta * kWarpStride + (MODE != AotMode::count ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0);
+  uint32_t words = kWarpsPerCta * kWarpStride + (MODE == AotMode::list ? kWarpsPerCta * 2 * emit_cap<MODE>() : 0);
   if (ring_mode<MODE>())
     words = ring_words_offset<MODE>() + ((kWarpsPerCta * 2 * kRingStages + 31) & ~31u) +
             kWarpsPerCta * kRingStages * kRingWords;
@@ -1908,6 +1970,13 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
   P.win = cwin;
   P.cs = cs;
   P.orig = og.orig.p;
+  if (mode == AotMode::hash && !og.vword.p && og.n) {  // the hash sink's vertex words, once per orientation
+    og.vword.alloc(og.n, s);
+    k_vertex_words<<<grid_for(og.n, 256, 148u * 64u), 256, 0, s>>>(og.orig.p, og.n, og.vword.p);
+    TL_CUDA(cudaGetLastError());
+    ++r.launches;
+  }
+  P.vword = og.vword.p;
   P.skip_neg = skip_negative;
   P.swap_neg = spec.algo == Algo::cf_hash;
   P.acc = acc.p;

@@ -120,6 +120,7 @@ tl_oriented::~tl_oriented() {
   claim_off.reset();
   win.reset();
   claim_s.reset();
+  vword.reset();
   fwd_win.reset();  // every buffer is freed on its stream before the stream goes
   cp.reset();
   plans.clear();

@@ -48,10 +48,25 @@ __host__ __device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t k) {
   return fmix64(seed + (k + 1) * kGolden);
 }
 
-// Order-independent triangle hash over a canonical (a<b<c) original-id
-// triple.
-__host__ __device__ __forceinline__ uint64_t tri_hash(uint32_t a, uint32_t b, uint32_t c) {
-  return fmix64(fmix64((uint64_t(a) << 32) | b) ^ uint64_t(c));
+// Order-independent triangle hash, round 2.  Every
+// vertex has a 64-bit word Z(v) = fmix64(v + golden) of its ORIGINAL id; a
+// triangle {a, b, c} contributes
+//     Z(a) * Z(b) * Z(c)  (mod 2^64)  to hash_sum   and
+//     Z(a) & Z(b) & Z(c)              to hash_xor,
+// both symmetric in the three ids (no canonical order needed) and both
+// distributive over their accumulation (+ resp. ^): the hits w of one claim
+// (l, s) add up to Z(l) Z(s) * sum Z(w) and (Z(l) & Z(s)) & xor Z(w), so the
+// hash sink of the device costs one gathered word and four integer
+// instructions per triangle instead of two 64-bit mixes, a three-way sort and
+// a staged compaction.  The reference side (oracle/ref_shim.cpp's HashSink
+// behind run_parallel) evaluates the same two expressions per emitted
+// triangle.
+__host__ __device__ __forceinline__ uint64_t vertex_word(uint32_t v) { return fmix64(uint64_t(v) + kGolden); }
+__host__ __device__ __forceinline__ uint64_t tri_hash_sum(uint32_t a, uint32_t b, uint32_t c) {
+  return vertex_word(a) * vertex_word(b) * vertex_word(c);
+}
+__host__ __device__ __forceinline__ uint64_t tri_hash_xor(uint32_t a, uint32_t b, uint32_t c) {
+  return vertex_word(a) & vertex_word(b) & vertex_word(c);
 }
 
 // canonical_triangle (reference graph.cpp:148-153).

@@ -54,6 +54,7 @@ struct tl_oriented {
   tlb::DBuf<uint64_t> claim_off;  // n+1, by pivot
   tlb::DBuf<uint64_t> win;        // m claim windows {begin:40 | len:23 | neg:1} into col
   tlb::DBuf<uint32_t> claim_s;    // m traversed vertex ids s | neg << 31
+  tlb::DBuf<uint64_t> vword;      // n: rank -> vertex_word(original id), the hash sink's table (built on first use)
   // forward claims (kclist3 / cf merge: pivot t traverses N+(h) for every
   // edge t->h; grouped by t = the out-CSR itself), built on first use
   tlb::DBuf<uint64_t> fwd_win;    // m windows {off[h] | deg+(h) << 40}

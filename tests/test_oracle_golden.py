@@ -177,10 +177,18 @@ def test_golden_c1_list_and_generators():
 
 
 def test_triangle_hash_definition():
-    # h = fmix64(fmix64(a << 32 | b) ^ c) over canonical a < b < c
+    # Z(v) = fmix64(v + golden); a triangle adds Z(a) Z(b) Z(c) mod 2^64 to hash_sum and
+    # xors Z(a) & Z(b) & Z(c) into hash_xor (symmetric: no canonical order needed)
+    M = (1 << 64) - 1
     a, b, c = 3, 17, 99
-    assert O.triangle_hash(a, b, c) == O.fmix64(O.fmix64((a << 32) | b) ^ c)
-    assert O.hash_of_triples(np.array([[a, b, c]], np.uint32))[1] == O.triangle_hash(a, b, c)
+    za, zb, zc = (O.fmix64((v + 0x9E3779B97F4A7C15) & M) for v in (a, b, c))
+    assert O.vertex_word(a) == za
+    assert O.triangle_hash(a, b, c) == (za * zb * zc) & M == O.triangle_hash(c, a, b)
+    assert O.triangle_hash_xor(a, b, c) == za & zb & zc == O.triangle_hash_xor(b, c, a)
+    cnt, hs, hx = O.hash_of_triples(np.array([[a, b, c], [1, 2, 3]], np.uint32))
+    assert cnt == 2
+    assert hs == (O.triangle_hash(a, b, c) + O.triangle_hash(1, 2, 3)) & M
+    assert hx == O.triangle_hash_xor(a, b, c) ^ O.triangle_hash_xor(1, 2, 3)
 
 
 def test_draw_is_sequential_splitmix64():

@@ -33,11 +33,12 @@ std::uint64_t fmix64(std::uint64_t z) {  // ordering.cpp:16-18
 struct HashSink {  // order-independent triangle hash
   std::uint64_t* acc;  // [count, sum, xor]
   void operator()(trilist::VertexId a, trilist::VertexId b, trilist::VertexId c) const {
-    const trilist::Triangle t = trilist::canonical_triangle(a, b, c);
-    const std::uint64_t h = fmix64(fmix64((std::uint64_t(t.a) << 32) | t.b) ^ t.c);
+    // Z(v) = fmix64(v + golden); sum of Z(a) Z(b) Z(c), xor of Z(a) & Z(b) & Z(c)
+    const std::uint64_t za = fmix64(a + 0x9E3779B97F4A7C15ull), zb = fmix64(b + 0x9E3779B97F4A7C15ull),
+                        zc = fmix64(c + 0x9E3779B97F4A7C15ull);
     acc[0] += 1;
-    acc[1] += h;
-    acc[2] ^= h;
+    acc[1] += za * zb * zc;
+    acc[2] ^= za & zb & zc;
   }
 };
 
