@@ -57,8 +57,9 @@ typedef struct tl_stats {
   uint64_t positive_triangles;
   uint64_t negative_triangles;
   uint64_t probes_executed;   /* probes left after rank-window early exit                          */
-  uint64_t hash_sum;          /* order-independent triangle hash, sum mod 2^64 (hash/list modes)   */
-  uint64_t hash_xor;          /*                                   xor                              */
+  uint64_t hash_sum;          /* order-independent triangle hash (hash mode): with Z(v) = fmix64(v +  */
+  uint64_t hash_xor;          /* 0x9E3779B97F4A7C15) of the original ids, sum of Z(a)Z(b)Z(c) mod 2^64  */
+                              /* and xor of Z(a)&Z(b)&Z(c) over the emitted triangles                  */
   uint64_t tasks;             /* work items scheduled                                              */
   double list_ms;             /* device time of the listing kernels (CUDA events)                  */
   double prep_ms;             /* device time of per-run task construction                          */

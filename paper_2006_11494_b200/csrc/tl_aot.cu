@@ -673,6 +673,12 @@ __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint
 #ifndef TL_PIPE
 #define TL_PIPE 1
 #endif
+#ifndef TL_PIPE_FULL
+#define TL_PIPE_FULL 0
+#endif
+#ifndef TL_PIPE_TAIL
+#define TL_PIPE_TAIL 0
+#endif
 #ifndef TL_PIPE_HASH
 #define TL_PIPE_HASH 0
 #endif
@@ -964,6 +970,24 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
         for (int k = 0; k < U; ++k) {
           zsum += z[k];
           zxor ^= z[k];
+        }
+      } else if (TL_PIPE_TAIL && stop && __all_sync(kFull, x[U / 2] == kEmpty)) {
+        // a list's last group with at most U/2 rounds of ids: the empty rounds are not probed
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          if (k < U / 2) {
+            if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
+            else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
+          }
+          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
+        }
+      } else if (TL_PIPE_FULL && __all_sync(kFull, 32 * (U - 1) < rem)) {
+        // the next group lies wholly inside its window: unpredicated reloads
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
+          else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
+          x[k] = __ldg(p + 32 * k);
         }
       } else {
 #pragma unroll
