@@ -673,15 +673,6 @@ __device__ __forceinline__ void emit_group(Lane<MODE>& st, const Params& P, uint
 #ifndef TL_PIPE
 #define TL_PIPE 1
 #endif
-#ifndef TL_PIPE_FULL
-#define TL_PIPE_FULL 0
-#endif
-#ifndef TL_PIPE_TAIL
-#define TL_PIPE_TAIL 0
-#endif
-#ifndef TL_PIPE_HASH
-#define TL_PIPE_HASH 0
-#endif
 template <AotMode MODE, int U>
 constexpr bool kOverLast() {
   return !(MODE == AotMode::count && U == kUnrollLong);
@@ -912,7 +903,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   // ---- long claims: the whole warp sweeps one list, U rounds of 32
   // loads in flight; lists are rank-ascending, so a list is abandoned once a
   // group reaches past max N+(l)
-  if constexpr (TL_PIPE && (MODE == AotMode::count || (TL_PIPE_HASH && MODE == AotMode::hash))) {
+  if constexpr (TL_PIPE && MODE == AotMode::count) {
     // Software-pipelined over the batch's long lists as one stream of groups:
     // a group's registers are reloaded with the next group -- of the same
     // list, or the first group of the next list once this one ends -- while
@@ -921,9 +912,9 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     // The group's last round decides the early exit first (ids ascend across
     // rounds and lanes; kEmpty past the window's end also ends the list),
     // which also orders all U loads of a group before their first use.
-    // Hash mode gathers a hit's vertex word before its id's register is
-    // reloaded and adds the group's words after the reloads are issued.  (List
-    // mode keeps the probed ids for the staged hits.)
+    // (Measured and left out, profiles/r2_sweep_count_pipeline.md: the same
+    // stream for hash mode, unpredicated reloads for groups wholly inside
+    // their window, skipping the empty rounds of a list's last group.)
     if (!longm) return;
     int j = __ffs(longm) - 1;
     longm &= longm - 1;
@@ -935,12 +926,10 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
 #pragma unroll
     for (int k = 0; k < U; ++k) x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
     uint32_t hits = 0, groups = 0;
-    unsigned long long zsum = 0, zxor = 0;  // hash mode: this lane's witnesses' words of the current list
     while (true) {
       const bool stop = __any_sync(kFull, x[U - 1] > lmax);  // the current list's last group
       const bool cneg = nj;
       const uint32_t lprev = lcur;
-      const int jprev = j;
       bool more = true;
       if (stop) {
         more = longm != 0;
@@ -957,54 +946,15 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
       }
       p += 32 * U;
       rem -= 32 * U;
-      if constexpr (MODE == AotMode::hash) {
-        unsigned long long z[U];
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const uint32_t hit = Probe::kRangeChecked ? probe.bit(x[k]) : uint32_t(x[k] <= lmax && probe.test(x[k]));
-          hits += hit;
-          z[k] = hit ? __ldg(P.vword + x[k]) : 0ull;
-          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          zsum += z[k];
-          zxor ^= z[k];
-        }
-      } else if (TL_PIPE_TAIL && stop && __all_sync(kFull, x[U / 2] == kEmpty)) {
-        // a list's last group with at most U/2 rounds of ids: the empty rounds are not probed
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          if (k < U / 2) {
-            if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
-            else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
-          }
-          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
-        }
-      } else if (TL_PIPE_FULL && __all_sync(kFull, 32 * (U - 1) < rem)) {
-        // the next group lies wholly inside its window: unpredicated reloads
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
-          else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
-          x[k] = __ldg(p + 32 * k);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
-          else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
-          x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
-        }
+      for (int k = 0; k < U; ++k) {
+        if constexpr (Probe::kRangeChecked) hits = probe.add(x[k], hits);
+        else hits += uint32_t(x[k] <= lmax && probe.test(x[k]));
+        x[k] = 32 * k < rem ? __ldg(p + 32 * k) : kEmpty;
       }
       ++groups;
       if (stop) {
         if (cneg) st.neg += hits; else st.pos += hits;
-        if constexpr (MODE == AotMode::hash) {
-          st.hsum += zsum * __shfl_sync(kFull, fmul, jprev);
-          st.hxor ^= zxor & __shfl_sync(kFull, fand, jprev);
-          zsum = zxor = 0;
-        }
         if (TL_EXEC_COUNT && lane == 0) red_add_sm64(exec_addr(), min(lprev, 32 * U * groups));  // ids loaded
         hits = 0;
         groups = 0;
