@@ -497,6 +497,11 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "bytes_per_launch": B["count"] // world, "peak_source": peaks["source"],
+                         # `achieved` counts ALGORITHMIC bytes (4 B per logical probe), part of
+                         # which the windowed traversal never loads or finds in L2, so frac can pass 1; the
+                         # DRAM-level figure is the ncu traffic of one launch over this run's kernel time
+                         "traffic_gbs": (traffic / world / (kern_ms * 1e-3) / 1e9) if traffic else None,
+                         "traffic_frac": (traffic / world / (kern_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]) if traffic else None,
                          "kernel": "k_aot (AOT intersection, both phases), CUDA events on the launch stream"},
             "cpu_baseline": cpu,
             "cpu_baseline_live_sample": cpu_live if anchor else None,
