@@ -13,15 +13,19 @@
 //     relabelled by rank, so N+(l) lies in [min, max] of its own ranks; when
 //     that span fits, the probe side is a direct bitmap over the span (the
 //     reference's bitmap, restricted to the window: one LDS + bit test per
-//     probe, no collision loop).  Wider spans fall back to an open-addressing
-//     hash (key + 1 stored, 0 = empty, so both layouts share the all-zero
-//     resting state).  Per warp: 8 KB (65,536-bit span or 2,048 slots); heavy
-//     pivots (deg+ > 1024 with a wide span) use a 128 KB per-CTA region, and a
-//     binary search over the sorted global list beyond that;
-//   * traversal lists are streamed with coalesced loads: lists longer than 32
-//     are swept by the whole warp (4 rounds in flight, early exit once a rank
-//     exceeds max N+(l) -- lists are rank-ascending), shorter ones are packed
-//     32 probes per round by a warp-level load-balanced search;
+//     probe, no collision loop).  Wider spans use a two-level rank bitmap, then
+//     hashes (key + 1 stored, 0 = empty, so every layout shares the all-zero
+//     resting state).  Per warp: 4.6 KB (a 37,888-bit span); heavy pivots with
+//     a wide span use the CTA's 38 KB, and a binary search over the sorted
+//     global list beyond that;
+//   * traversal lists are streamed with coalesced loads: lists longer than 64
+//     are swept by the whole warp (4 or 8 rounds in flight, early exit once a
+//     rank exceeds max N+(l) -- lists are rank-ascending; count mode sweeps a
+//     batch's long lists as one software-pipelined stream), shorter ones are
+//     packed 32 probes per round by a warp-level load-balanced search;
+//   * hash mode accumulates, per claim, the sum and the xor of its witnesses'
+//     vertex words (tl_common.cuh: the hash distributes over a claim's hits);
+//     list mode stages hits per warp and flushes them per pivot;
 //   * work is described by compact records (one per pivot with work, or per
 //     chunk of a heavy pivot's claim list cut at the claim-cost prefix) and
 //     cost-balanced tasks over consecutive records, fetched dynamically; the
@@ -46,8 +50,8 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // padding value of an out-of-range lo
 
 // Tuning knobs (compile-time; see tools/sweep.py):
 // Rounds of 32 traversal loads in flight per warp: 4 for graphs whose mean
-// window is short (L2-resident C2, C3), 6 for long windows (C4, C5), chosen
-// per run from the mean window length.
+// window is short (L2-resident C2, C3), 8 for long windows (C4, C5; 6 in the
+// emission modes), chosen per run from the mean window length.
 #ifndef TL_UNROLL
 #define TL_UNROLL 4
 #endif
