@@ -207,6 +207,7 @@ struct Params {
   const Rec* crecs;     // phase 1 (CTA) records, one per task
   uint64_t ncta;
   uint32_t skip_neg;
+  uint32_t prefetch;    // L2 prefetches of the batch's windows: on when the out-lists do not fit in L2
   uint32_t swap_neg;    // cf-hash: a negative claim emits (tail, head, w) (engine.hpp:212)
   unsigned long long* acc;
   uint32_t* out;
@@ -831,7 +832,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
   // demand loads find them there or on their way: more bytes in flight per
   // warp without holding registers.
   auto prefetch_list = [&](unsigned m) {
-    if (m) {
+    if (m && P.prefetch) {
       const int jn = __ffs(m) - 1;
       const uint64_t bn = __shfl_sync(kFull, b, jn);
       const uint32_t ln = __shfl_sync(kFull, len, jn);
@@ -839,7 +840,7 @@ __device__ __forceinline__ void claim_batch(const Params& P, const Probe& probe,
     }
   };
   if (TL_PREFETCH >= 2) prefetch_list(__ballot_sync(kFull, len > kShort));  // the first long list, under the packed rounds
-  if (TL_PREFETCH >= 3 && len && len <= kShort) {  // the packed claims' lines (rounds after the first find them in L2)
+  if (TL_PREFETCH >= 3 && P.prefetch && len && len <= kShort) {  // the packed claims' lines (rounds after the first find them in L2)
     prefetch_l2(P.col + b);
     prefetch_l2(P.col + b + len - 1);
   }
@@ -1955,6 +1956,14 @@ AotResult aot_run(tl_oriented& og, const RunSpec& spec, cudaStream_t s, uint32_t
     ++r.launches;
   }
   P.vword = og.vword.p;
+  {  // an L2-resident CSR (C2) gains nothing from L2 prefetches and pays their issue slots (C2 list +3%)
+    static int l2_bytes[64] = {0};
+    int dev = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    int& l2 = l2_bytes[dev >= 0 && dev < 64 ? dev : 0];
+    if (!l2) TL_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    P.prefetch = 4 * m > uint64_t(l2) ? 1u : 0u;
+  }
   P.skip_neg = skip_negative;
   P.swap_neg = spec.algo == Algo::cf_hash;
   P.acc = acc.p;
